@@ -1,0 +1,684 @@
+// capi.cu -- implementation of the C-ABI declared in include/countdown_b200.h.
+//
+// Owns the per-layer device state (re-laid-out weights, self-cleaning scratch, a stream,
+// pinned staging for the host-buffer entry points) and sequences the kernel chains of
+// kernels_fast.cu (UnorderedAccumulate) and kernels_exact.cu (DeterministicOrdered).
+// No CPU compute path exists: every operator runs on the device or fails.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/countdown_b200.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+    g_err = msg;
+    throw Fail{code};
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(CD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F> int guarded(F&& f) {
+    try {
+        f();
+        return CD_OK;
+    } catch (const Fail& e) {
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return CD_ERR_USAGE;
+    }
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+struct cd_layer {
+    int device = 0;
+    int num_sms = 148;
+    cdk::LayerDev L;
+    cdk::Scratch S;
+    int64_t F_total = 0, row_begin = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    std::vector<void*> dev_allocs;
+    std::vector<void*> host_allocs;
+    int64_t bytes = 0;
+    int last_launches = 0;
+    // device staging for the host-buffer entry points
+    float* d_x = nullptr;
+    float* d_y = nullptr;
+    uint8_t* d_mask_in = nullptr;
+    uint8_t* d_mask_out = nullptr;
+    float* d_u_in = nullptr;
+    float* d_ind = nullptr;
+    int* d_alive = nullptr;
+    // pinned host staging
+    float* h_x = nullptr;
+    float* h_y = nullptr;
+    uint8_t* h_mask = nullptr;
+    float* h_ind = nullptr;
+    int* h_alive = nullptr;
+
+    template <typename T> T* dalloc(size_t n, bool zero = true) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+        dev_allocs.push_back(p);
+        bytes += static_cast<int64_t>(n * sizeof(T));
+        if (zero) ck(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)), "cudaMemset");
+        return static_cast<T*>(p);
+    }
+    template <typename T> T* halloc(size_t n) {
+        void* p = nullptr;
+        ck(cudaMallocHost(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMallocHost");
+        host_allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~cd_layer() {
+        if (stream) {
+            cudaSetDevice(device);
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+        }
+        for (void* p : dev_allocs) cudaFree(p);
+        for (void* p : host_allocs) cudaFreeHost(p);
+    }
+};
+
+namespace {
+
+using cdk::kMaxBatch;
+using cdk::kMaxBatchFast;
+
+// Upload rows [row_begin, row_end) of a full host matrix (rows x cols f32) into a padded
+// device matrix (dtype, row stride ld), via an f32 staging buffer and the pack kernel.
+void upload_rows(cd_layer* h, const float* host, int64_t row_begin, int64_t nrows, int64_t cols,
+                 void* dst, int64_t ld, float* tmp) {
+    ck(cudaMemcpyAsync(tmp, host + row_begin * cols, sizeof(float) * nrows * cols,
+                       cudaMemcpyHostToDevice, h->stream),
+       "upload");
+    ck(cdk::launch_pack_rows(tmp, nrows, cols, cols, dst, h->L.dtype, ld, h->stream), "pack_rows");
+}
+
+struct Req {
+    int method = cdk::kDC;
+    bool with_masks = false;  // exec_mc / exec_dc: caller-supplied masks
+    int nb = 1;
+    const float* x = nullptr;
+    float tau = 0.0f;
+    int reduction = CD_REDUCTION_UNORDERED;
+    const uint8_t* ovr = nullptr;       // DC mask override
+    const uint8_t* masks_in = nullptr;  // exec masks
+    const float* u_in = nullptr;        // exec_mc u
+    float* y = nullptr;
+    uint8_t* mask_out = nullptr;
+    float* ind_out = nullptr;
+    int* alive_out = nullptr;
+    cudaStream_t stream = nullptr;
+};
+
+// Enqueue one operator call (device pointers) on r.stream.  Returns the number of launches.
+int run_chain(cd_layer* h, const Req& r) {
+    const cdk::LayerDev& L = h->L;
+    const cdk::Scratch& S = h->S;
+    cdk::LaunchCfg c;
+    c.num_sms = h->num_sms;
+    c.stream = r.stream ? r.stream : h->stream;
+    const int64_t d = L.d, F = L.F;
+    int launches = 0;
+    if (r.method == cdk::kDC && !r.with_masks && !L.theta_bt)
+        fail(CD_ERR_DATA, "pipeline_dc: layer has no low-rank predictor attached");
+    if (!L.w_up) fail(CD_ERR_DATA, "forward: handle holds only a predictor (no layer weights)");
+
+    if (r.reduction == CD_REDUCTION_UNORDERED) {
+        for (int c0 = 0; c0 < r.nb; c0 += kMaxBatchFast) {
+            const int n = std::min(kMaxBatchFast, r.nb - c0);
+            const float* xc = r.x + c0 * d;
+            float* yc = r.y + c0 * d;
+            uint8_t* mo = r.mask_out ? r.mask_out + c0 * F : nullptr;
+            float* io = r.ind_out ? r.ind_out + c0 * F : nullptr;
+            int* ao = r.alive_out ? r.alive_out + c0 : nullptr;
+            if (r.with_masks) {
+                ck(cdk::launch_compact_masks(L, S, r.masks_in + c0 * F,
+                                             r.method == cdk::kMC ? r.u_in + c0 * F : nullptr, n, yc, c),
+                   "compact_masks");
+                ck(cdk::launch_sparse_fast(L, S, r.method, false, xc, n, yc, ao, c), "sparse");
+                launches += 2;
+            } else if (r.method == cdk::kDense) {
+                ck(cdk::launch_sparse_fast(L, S, cdk::kDC, true, xc, n, yc, ao, c), "dense");
+                launches += 2;
+            } else if (r.method == cdk::kMC) {
+                ck(cdk::launch_indicator_mc_fast(L, S, xc, n, r.tau, yc, mo, io, c), "indicator_mc");
+                ck(cdk::launch_sparse_fast(L, S, cdk::kMC, false, xc, n, yc, ao, c), "sparse_mc");
+                launches += 2;
+            } else {
+                ck(cdk::launch_latent_fast(L, S, xc, n, c), "latent");
+                ck(cdk::launch_indicator_dc_fast(L, S, n, r.tau, r.ovr ? r.ovr + c0 * F : nullptr, yc, mo, io, c),
+                   "indicator_dc");
+                ck(cdk::launch_sparse_fast(L, S, cdk::kDC, false, xc, n, yc, ao, c), "sparse_dc");
+                launches += 3;
+            }
+        }
+        return launches;
+    }
+
+    // ---- DeterministicOrdered: bitwise reference folds.
+    for (int c0 = 0; c0 < r.nb; c0 += kMaxBatch) {
+        const int n = std::min(kMaxBatch, r.nb - c0);
+        const float* xc = r.x + c0 * d;
+        float* yc = r.y + c0 * d;
+        uint8_t* mo = r.mask_out ? r.mask_out + c0 * F : nullptr;
+        int* ao = r.alive_out ? r.alive_out + c0 : nullptr;
+        float* ind = r.ind_out ? r.ind_out + c0 * F : S.ind;
+        const float* u_full = nullptr;
+        if (r.with_masks) {
+            if (r.method == cdk::kMC) u_full = r.u_in + c0 * F;
+            ck(cdk::launch_exact_compact(L, S, 2, nullptr, r.masks_in + c0 * F, n, 0.0f, mo, ao, c), "compact");
+            launches += 1;
+        } else if (r.method == cdk::kDense) {
+            ck(cdk::launch_exact_compact(L, S, 3, nullptr, nullptr, n, 0.0f, mo, ao, c), "compact");
+            launches += 1;
+        } else if (r.method == cdk::kMC) {
+            ck(cdk::launch_exact_rowdot_all(L.w_up, L.dtype, F, L.ld, d, xc, d, n, ind, F, c), "rowdot_up");
+            ck(cdk::launch_exact_compact(L, S, 0, ind, nullptr, n, r.tau, mo, ao, c), "compact");
+            u_full = ind;
+            launches += 2;
+        } else {
+            ck(cdk::launch_exact_latent(L, S, xc, n, c), "latent_exact");
+            ck(cdk::launch_exact_rowdot_all(L.theta_bt, L.dtype, F, L.ldr, L.r, S.ex_lat, L.ldr, n, ind, F, c),
+               "logits_exact");
+            if (r.ovr)
+                ck(cdk::launch_exact_compact(L, S, 2, nullptr, r.ovr + c0 * F, n, 0.0f, mo, ao, c), "compact");
+            else
+                ck(cdk::launch_exact_compact(L, S, 1, ind, nullptr, n, r.tau, mo, ao, c), "compact");
+            launches += 3;
+        }
+        const int m = r.method == cdk::kDense ? cdk::kDC : r.method;
+        ck(cdk::launch_exact_phase1(L, S, m, xc, u_full, n, c), "phase1");
+        ck(cdk::launch_exact_down(L, S, n, yc, c), "down");
+        launches += 2;
+        // restore the self-cleaning scratch the fast chain relies on
+        ck(cudaMemsetAsync(S.count, 0, sizeof(int), c.stream), "memset");
+        ck(cudaMemsetAsync(S.alive, 0, sizeof(int) * kMaxBatch, c.stream), "memset");
+    }
+    return launches;
+}
+
+void check_layer(const cd_layer* h) {
+    if (!h) fail(CD_ERR_DATA, "null layer handle");
+}
+
+void check_common(const cd_layer* h, int64_t batch, const float* x, const float* y) {
+    check_layer(h);
+    if (batch <= 0) fail(CD_ERR_DATA, "batch must be positive");
+    if (!x) fail(CD_ERR_DATA, "x is null");
+    if (!y) fail(CD_ERR_DATA, "y is null");
+}
+
+void check_reduction(int reduction) {
+    if (reduction != CD_REDUCTION_ORDERED && reduction != CD_REDUCTION_UNORDERED)
+        fail(CD_ERR_DATA, "unknown reduction mode");
+}
+
+// Host-buffer call: stage through pinned memory in chunks of kMaxBatch samples.
+struct HostIO {
+    const float* x = nullptr;
+    const uint8_t* masks_in = nullptr;
+    const uint8_t* ovr = nullptr;
+    const float* u_in = nullptr;
+    float* y = nullptr;
+    uint8_t* mask_out = nullptr;
+    float* ind_out = nullptr;
+    int64_t* alive_out = nullptr;
+};
+
+void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
+    std::lock_guard<std::mutex> g(h->mu);
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    const int64_t d = h->L.d, F = h->L.F;
+    cudaStream_t s = h->stream;
+    int launches = 0;
+    for (int64_t c0 = 0; c0 < batch; c0 += kMaxBatch) {
+        const int n = static_cast<int>(std::min<int64_t>(kMaxBatch, batch - c0));
+        std::memcpy(h->h_x, io.x + c0 * d, sizeof(float) * n * d);
+        ck(cudaMemcpyAsync(h->d_x, h->h_x, sizeof(float) * n * d, cudaMemcpyHostToDevice, s), "H2D x");
+        const uint8_t* masks = io.masks_in ? io.masks_in : io.ovr;
+        if (masks) {
+            std::memcpy(h->h_mask, masks + c0 * F, static_cast<size_t>(n * F));
+            ck(cudaMemcpyAsync(h->d_mask_in, h->h_mask, n * F, cudaMemcpyHostToDevice, s), "H2D mask");
+        }
+        if (io.u_in) {
+            std::memcpy(h->h_ind, io.u_in + c0 * F, sizeof(float) * n * F);
+            ck(cudaMemcpyAsync(h->d_u_in, h->h_ind, sizeof(float) * n * F, cudaMemcpyHostToDevice, s), "H2D u");
+        }
+        // pinned staging is reused below: make sure the uploads have consumed it
+        Req r = base;
+        r.nb = n;
+        r.x = h->d_x;
+        r.y = h->d_y;
+        r.masks_in = io.masks_in ? h->d_mask_in : nullptr;
+        r.ovr = io.ovr ? h->d_mask_in : nullptr;
+        r.u_in = io.u_in ? h->d_u_in : nullptr;
+        r.mask_out = io.mask_out ? h->d_mask_out : nullptr;
+        r.ind_out = io.ind_out ? h->d_ind : nullptr;
+        r.alive_out = h->d_alive;
+        r.stream = s;
+        launches += run_chain(h, r);
+        ck(cudaMemcpyAsync(h->h_y, h->d_y, sizeof(float) * n * d, cudaMemcpyDeviceToHost, s), "D2H y");
+        ck(cudaMemcpyAsync(h->h_alive, h->d_alive, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "D2H alive");
+        if (io.mask_out)
+            ck(cudaMemcpyAsync(h->h_mask, h->d_mask_out, n * F, cudaMemcpyDeviceToHost, s), "D2H mask");
+        if (io.ind_out)
+            ck(cudaMemcpyAsync(h->h_ind, h->d_ind, sizeof(float) * n * F, cudaMemcpyDeviceToHost, s), "D2H ind");
+        ck(cudaStreamSynchronize(s), "forward");
+        std::memcpy(io.y + c0 * d, h->h_y, sizeof(float) * n * d);
+        if (io.mask_out) std::memcpy(io.mask_out + c0 * F, h->h_mask, static_cast<size_t>(n * F));
+        if (io.ind_out) std::memcpy(io.ind_out + c0 * F, h->h_ind, sizeof(float) * n * F);
+        if (io.alive_out)
+            for (int b = 0; b < n; ++b) io.alive_out[c0 + b] = h->h_alive[b];
+    }
+    h->last_launches = launches;
+}
+
+cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_t re, int act,
+                      int dtype, const float* w_up, const float* w_gate, const float* w_down,
+                      bool predictor_only = false) {
+    if (d <= 0 || F_total <= 0) {
+        fail(CD_ERR_DATA, "layer: bad dims d_model=" + std::to_string(d) + " d_inter=" + std::to_string(F_total));
+    }
+    if (rb < 0 || re > F_total || re <= rb) fail(CD_ERR_DATA, "layer: bad shard row range");
+    if (act != CD_ACT_SILU && act != CD_ACT_GELU_TANH) fail(CD_ERR_DATA, "layer: unknown activation");
+    if (dtype != CD_DTYPE_F32 && dtype != CD_DTYPE_BF16) fail(CD_ERR_DATA, "layer: unknown dtype");
+    if (!predictor_only && (!w_up || !w_gate || !w_down)) fail(CD_ERR_DATA, "layer: null weight pointer");
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) fail(CD_ERR_CUDA, "no such CUDA device");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        fail(CD_ERR_CUDA, "libcountdown_b200 is built for sm_100a (B200); device is sm_" +
+                              std::to_string(prop.major) + std::to_string(prop.minor));
+
+    auto h = std::make_unique<cd_layer>();
+    h->device = device;
+    h->num_sms = prop.multiProcessorCount;
+    ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cdk::LayerDev& L = h->L;
+    L.d = d;
+    L.F = re - rb;
+    L.ld = round_up(d, cdk::kVecElems);
+    L.act = act;
+    L.dtype = dtype;
+    h->F_total = F_total;
+    h->row_begin = rb;
+    const size_t esz = dtype == CD_DTYPE_BF16 ? 2 : 4;
+    const size_t nw = static_cast<size_t>(L.F * L.ld);
+    if (!predictor_only) {
+    void* wu = h->dalloc<uint8_t>(nw * esz, false);
+    void* wg = h->dalloc<uint8_t>(nw * esz, false);
+    void* wd = h->dalloc<uint8_t>(nw * esz, false);
+    float* tmp = nullptr;
+    ck(cudaMalloc(&tmp, sizeof(float) * L.F * d), "cudaMalloc tmp");
+    try {
+        upload_rows(h.get(), w_up, rb, L.F, d, wu, L.ld, tmp);
+        upload_rows(h.get(), w_gate, rb, L.F, d, wg, L.ld, tmp);
+        upload_rows(h.get(), w_down, rb, L.F, d, wd, L.ld, tmp);
+        ck(cudaStreamSynchronize(h->stream), "upload");
+    } catch (...) {
+        cudaFree(tmp);
+        throw;
+    }
+    cudaFree(tmp);
+    L.w_up = wu;
+    L.w_gate = wg;
+    L.w_down = wd;
+    }
+
+    cdk::Scratch& S = h->S;
+    S.list = h->dalloc<int32_t>(L.F);
+    S.bits = h->dalloc<uint32_t>(L.F);
+    S.list_val = h->dalloc<float>(L.F * kMaxBatchFast);
+    S.count = h->dalloc<int>(1);
+    S.done = h->dalloc<int>(1);
+    S.alive = h->dalloc<int>(kMaxBatch);
+    S.ind = h->dalloc<float>(kMaxBatch * L.F);
+    S.ex_s = h->dalloc<float>(kMaxBatch * L.F);
+    h->d_x = h->dalloc<float>(kMaxBatch * d);
+    h->d_y = h->dalloc<float>(kMaxBatch * d);
+    h->d_mask_in = h->dalloc<uint8_t>(kMaxBatch * L.F);
+    h->d_mask_out = h->dalloc<uint8_t>(kMaxBatch * L.F);
+    h->d_u_in = h->dalloc<float>(kMaxBatch * L.F);
+    h->d_ind = h->dalloc<float>(kMaxBatch * L.F);
+    h->d_alive = h->dalloc<int>(kMaxBatch);
+    h->h_x = h->halloc<float>(kMaxBatch * d);
+    h->h_y = h->halloc<float>(kMaxBatch * d);
+    h->h_mask = h->halloc<uint8_t>(kMaxBatch * L.F);
+    h->h_ind = h->halloc<float>(kMaxBatch * L.F);
+    h->h_alive = h->halloc<int>(kMaxBatch);
+    return h.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cd_last_error(void) { return g_err.c_str(); }
+
+int cd_version(void) { return 1; }
+
+int cd_device_info(int device, int* num_sms, int* cc_major, int* cc_minor) {
+    return guarded([&] {
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (num_sms) *num_sms = prop.multiProcessorCount;
+        if (cc_major) *cc_major = prop.major;
+        if (cc_minor) *cc_minor = prop.minor;
+    });
+}
+
+int cd_layer_create(int device, int64_t d_model, int64_t d_inter, int activation, int dtype,
+                    const float* w_up, const float* w_gate, const float* w_down, cd_layer** out) {
+    return guarded([&] {
+        if (!out) fail(CD_ERR_DATA, "out is null");
+        *out = create_impl(device, d_model, d_inter, 0, d_inter, activation, dtype, w_up, w_gate, w_down);
+    });
+}
+
+int cd_layer_create_shard(int device, int64_t d_model, int64_t d_inter_total, int64_t row_begin,
+                          int64_t row_end, int activation, int dtype, const float* w_up,
+                          const float* w_gate, const float* w_down, cd_layer** out) {
+    return guarded([&] {
+        if (!out) fail(CD_ERR_DATA, "out is null");
+        *out = create_impl(device, d_model, d_inter_total, row_begin, row_end, activation, dtype, w_up,
+                           w_gate, w_down);
+    });
+}
+
+int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, const float* theta_b) {
+    return guarded([&] {
+        check_layer(h);
+        if (d_rank <= 0) fail(CD_ERR_DATA, "make_lowrank_predictor: dims must be positive");
+        if (!theta_a || !theta_b) fail(CD_ERR_DATA, "predictor: null theta pointer");
+        std::lock_guard<std::mutex> g(h->mu);
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        cdk::LayerDev& L = h->L;
+        const int64_t ldr = round_up(d_rank, cdk::kVecElems);
+        if (ldr / cdk::kVecElems > 256) fail(CD_ERR_DATA, "predictor: d_rank > 2048 is not supported");
+        const size_t esz = L.dtype == CD_DTYPE_BF16 ? 2 : 4;
+        void* ta = h->dalloc<uint8_t>(static_cast<size_t>(L.d * ldr) * esz, false);
+        void* tbt = h->dalloc<uint8_t>(static_cast<size_t>(L.F * ldr) * esz, false);
+        float* tmp = nullptr;
+        const size_t tmp_n = static_cast<size_t>(std::max(L.d * d_rank, d_rank * h->F_total));
+        ck(cudaMalloc(&tmp, sizeof(float) * tmp_n), "cudaMalloc tmp");
+        cudaError_t e = cudaMemcpyAsync(tmp, theta_a, sizeof(float) * L.d * d_rank, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess) e = cdk::launch_pack_rows(tmp, L.d, d_rank, d_rank, ta, L.dtype, ldr, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(tmp, theta_b, sizeof(float) * d_rank * h->F_total, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess)
+            e = cdk::launch_pack_transpose(tmp, d_rank, h->F_total, h->row_begin, L.F, tbt, L.dtype, ldr, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        cudaFree(tmp);
+        ck(e, "predictor upload");
+        if (!h->S.latent) h->S.latent = h->dalloc<float>(kMaxBatch * 2048);
+        if (!h->S.ex_lat) h->S.ex_lat = h->dalloc<float>(kMaxBatch * 2048);
+        L.r = d_rank;
+        L.ldr = ldr;
+        L.theta_a = ta;
+        L.theta_bt = tbt;
+    });
+}
+
+int cd_layer_destroy(cd_layer* h) {
+    return guarded([&] { delete h; });
+}
+
+int cd_layer_shape(const cd_layer* h, int64_t* d_model, int64_t* d_inter, int64_t* d_rank, int* dtype,
+                   int* activation) {
+    return guarded([&] {
+        check_layer(h);
+        if (d_model) *d_model = h->L.d;
+        if (d_inter) *d_inter = h->L.F;
+        if (d_rank) *d_rank = h->L.r;
+        if (dtype) *dtype = h->L.dtype;
+        if (activation) *activation = h->L.act;
+    });
+}
+
+int cd_layer_device_bytes(const cd_layer* h, int64_t* bytes) {
+    return guarded([&] {
+        check_layer(h);
+        *bytes = h->bytes;
+    });
+}
+
+int cd_layer_last_launches(const cd_layer* h, int* launches) {
+    return guarded([&] {
+        check_layer(h);
+        *launches = h->last_launches;
+    });
+}
+
+int cd_exec_dense(cd_layer* h, int64_t batch, const float* x, int reduction, float* y) {
+    return guarded([&] {
+        check_common(h, batch, x, y);
+        check_reduction(reduction);
+        Req r;
+        r.method = cdk::kDense;
+        r.reduction = reduction;
+        HostIO io;
+        io.x = x;
+        io.y = y;
+        host_call(h, r, batch, io);
+    });
+}
+
+int cd_exec_mc(cd_layer* h, int64_t batch, const float* x, const float* u, const uint8_t* mask,
+               int reduction, float* y) {
+    return guarded([&] {
+        check_common(h, batch, x, y);
+        check_reduction(reduction);
+        if (!u || !mask) fail(CD_ERR_DATA, "exec_mc: u and mask are required");
+        Req r;
+        r.method = cdk::kMC;
+        r.with_masks = true;
+        r.reduction = reduction;
+        HostIO io;
+        io.x = x;
+        io.y = y;
+        io.u_in = u;
+        io.masks_in = mask;
+        host_call(h, r, batch, io);
+    });
+}
+
+int cd_exec_dc(cd_layer* h, int64_t batch, const float* x, const uint8_t* mask, int reduction, float* y) {
+    return guarded([&] {
+        check_common(h, batch, x, y);
+        check_reduction(reduction);
+        if (!mask) fail(CD_ERR_DATA, "exec_dc: mask is required");
+        Req r;
+        r.method = cdk::kDC;
+        r.with_masks = true;
+        r.reduction = reduction;
+        HostIO io;
+        io.x = x;
+        io.y = y;
+        io.masks_in = mask;
+        host_call(h, r, batch, io);
+    });
+}
+
+int cd_pipeline_mc(cd_layer* h, int64_t batch, const float* x, float tau, int reduction, float* y,
+                   uint8_t* mask_out, int64_t* alive_out, float* u_out) {
+    return guarded([&] {
+        check_common(h, batch, x, y);
+        check_reduction(reduction);
+        Req r;
+        r.method = cdk::kMC;
+        r.tau = tau;
+        r.reduction = reduction;
+        HostIO io;
+        io.x = x;
+        io.y = y;
+        io.mask_out = mask_out;
+        io.alive_out = alive_out;
+        io.ind_out = u_out;
+        host_call(h, r, batch, io);
+    });
+}
+
+int cd_pipeline_dc(cd_layer* h, int64_t batch, const float* x, float tau_d, const uint8_t* mask_override,
+                   int reduction, float* y, uint8_t* mask_out, int64_t* alive_out, float* logits_out) {
+    return guarded([&] {
+        check_common(h, batch, x, y);
+        check_reduction(reduction);
+        if (!h->L.theta_bt) fail(CD_ERR_DATA, "pipeline_dc: layer has no low-rank predictor attached");
+        Req r;
+        r.method = cdk::kDC;
+        r.tau = tau_d;
+        r.reduction = reduction;
+        HostIO io;
+        io.x = x;
+        io.y = y;
+        io.ovr = mask_override;
+        io.mask_out = mask_out;
+        io.alive_out = alive_out;
+        io.ind_out = logits_out;
+        host_call(h, r, batch, io);
+    });
+}
+
+int cd_predict_logits(cd_layer* h, int64_t batch, const float* x, float* logits) {
+    return guarded([&] {
+        check_layer(h);
+        if (batch <= 0 || !x || !logits) fail(CD_ERR_DATA, "predict_logits: bad arguments");
+        if (!h->L.theta_bt) fail(CD_ERR_DATA, "predict_logits: layer has no low-rank predictor attached");
+        std::lock_guard<std::mutex> g(h->mu);
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        const cdk::LayerDev& L = h->L;
+        cdk::LaunchCfg c;
+        c.num_sms = h->num_sms;
+        c.stream = h->stream;
+        for (int64_t c0 = 0; c0 < batch; c0 += kMaxBatch) {
+            const int n = static_cast<int>(std::min<int64_t>(kMaxBatch, batch - c0));
+            std::memcpy(h->h_x, x + c0 * L.d, sizeof(float) * n * L.d);
+            ck(cudaMemcpyAsync(h->d_x, h->h_x, sizeof(float) * n * L.d, cudaMemcpyHostToDevice, h->stream), "H2D");
+            ck(cdk::launch_exact_latent(L, h->S, h->d_x, n, c), "latent");
+            ck(cdk::launch_exact_rowdot_all(L.theta_bt, L.dtype, L.F, L.ldr, L.r, h->S.ex_lat, L.ldr, n, h->d_ind,
+                                            L.F, c),
+               "logits");
+            ck(cudaMemcpyAsync(h->h_ind, h->d_ind, sizeof(float) * n * L.F, cudaMemcpyDeviceToHost, h->stream), "D2H");
+            ck(cudaStreamSynchronize(h->stream), "predict_logits");
+            std::memcpy(logits + c0 * L.F, h->h_ind, sizeof(float) * n * L.F);
+        }
+        h->last_launches = 2;
+    });
+}
+
+int cd_forward_device(cd_layer* h, int method, int64_t batch, const float* d_x, float tau, int reduction,
+                      const uint8_t* d_mask_override, float* d_y, uint8_t* d_mask, float* d_indicator,
+                      int32_t* d_alive, void* stream) {
+    return guarded([&] {
+        check_common(h, batch, d_x, d_y);
+        check_reduction(reduction);
+        if (method != CD_METHOD_DENSE && method != CD_METHOD_MC && method != CD_METHOD_DC)
+            fail(CD_ERR_DATA, "unknown method");
+        if (d_mask_override && method != CD_METHOD_DC) fail(CD_ERR_DATA, "mask override is DC-only");
+        std::lock_guard<std::mutex> g(h->mu);
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        Req r;
+        r.method = method;
+        r.nb = static_cast<int>(batch);
+        r.x = d_x;
+        r.tau = tau;
+        r.reduction = reduction;
+        r.ovr = d_mask_override;
+        r.y = d_y;
+        r.mask_out = d_mask;
+        r.ind_out = d_indicator;
+        r.alive_out = d_alive;
+        r.stream = static_cast<cudaStream_t>(stream);
+        h->last_launches = run_chain(h, r);
+    });
+}
+
+int cd_predictor_create(int device, int64_t d_model, int64_t d_rank, int64_t d_inter, int dtype,
+                        const float* theta_a, const float* theta_b, cd_layer** out) {
+    return guarded([&] {
+        if (!out) fail(CD_ERR_DATA, "out is null");
+        std::unique_ptr<cd_layer> h(create_impl(device, d_model, d_inter, 0, d_inter, CD_ACT_SILU, dtype,
+                                                nullptr, nullptr, nullptr, true));
+        const int rc = cd_layer_set_predictor(h.get(), d_rank, theta_a, theta_b);
+        if (rc != CD_OK) throw Fail{rc};
+        *out = h.release();
+    });
+}
+
+int cd_bench_device(cd_layer* h, int method, int64_t batch, const float* x, float tau, int reduction,
+                    int64_t warmup, int64_t iters, int64_t* ns_out) {
+    return guarded([&] {
+        check_layer(h);
+        if (batch <= 0 || batch > kMaxBatch) fail(CD_ERR_DATA, "bench: batch must be in [1, 32]");
+        if (!x || !ns_out || iters <= 0 || warmup < 0) fail(CD_ERR_DATA, "bench: iters must be positive");
+        check_reduction(reduction);
+        std::lock_guard<std::mutex> g(h->mu);
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        cudaStream_t s = h->stream;
+        ck(cudaMemcpyAsync(h->d_x, x, sizeof(float) * batch * h->L.d, cudaMemcpyHostToDevice, s), "H2D x");
+        Req r;
+        r.method = method;
+        r.nb = static_cast<int>(batch);
+        r.x = h->d_x;
+        r.tau = tau;
+        r.reduction = reduction;
+        r.y = h->d_y;
+        r.alive_out = h->d_alive;
+        r.stream = s;
+        for (int64_t i = 0; i < warmup; ++i) run_chain(h, r);
+        cudaEvent_t e0, e1;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        cudaError_t err = cudaSuccess;
+        for (int64_t i = 0; i < iters && err == cudaSuccess; ++i) {
+            cudaEventRecord(e0, s);
+            h->last_launches = run_chain(h, r);
+            cudaEventRecord(e1, s);
+            err = cudaEventSynchronize(e1);
+            float ms = 0.0f;
+            if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, e0, e1);
+            ns_out[i] = static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        ck(err, "bench");
+    });
+}
+
+int cd_layer_sync(cd_layer* h) {
+    return guarded([&] {
+        check_layer(h);
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(h->stream), "sync");
+    });
+}
+
+}  // extern "C"

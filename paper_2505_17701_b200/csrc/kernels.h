@@ -1,0 +1,111 @@
+// kernels.h -- host-side launch interface of the COUNTDOWN sm_100a kernels.
+//
+// Device data layout (one layer / one tensor-parallel shard), all in HBM:
+//   w_up, w_gate, w_down : F x ld, neuron-major row-major (gated_mlp.hpp:16-19 layout), ld =
+//                          round_up(d, 8) zero-padded so every row is a whole number of
+//                          16-byte vectors -> one contiguous run per neuron for the TMA engine.
+//   theta_a              : d x ldr (reference layout, predictor.hpp:17), ldr = round_up(r, 8).
+//   theta_bt             : F x ldr, theta_b (r x F, predictor.hpp:18) transposed so one
+//                          neuron's predictor row is contiguous.
+// Weights are f32 (oracle mode) or bf16 (RNE-rounded, perf mode); x, y, and all
+// accumulation are f32.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cdk {
+
+constexpr int kVecElems = 8;      // weights per 16-byte (bf16) vector unit; row stride multiple
+constexpr int kMaxBatchFast = 4;   // samples per fused-kernel instance (union of masks)
+constexpr int kMaxBatch = 32;      // samples per call (bitmask width)
+
+struct LayerDev {
+    int64_t d = 0, F = 0, ld = 0;  // d_model, rows in this shard, padded row stride
+    int act = 0, dtype = 0;
+    const void* w_up = nullptr;
+    const void* w_gate = nullptr;
+    const void* w_down = nullptr;
+    int64_t r = 0, ldr = 0;
+    const void* theta_a = nullptr;   // d x ldr
+    const void* theta_bt = nullptr;  // F x ldr
+};
+
+// Per-handle device scratch.  latent/count/done are "self-cleaning": every kernel
+// chain leaves them zero for the next one (initialised by cudaMemset at creation).
+struct Scratch {
+    float* latent = nullptr;       // kMaxBatch x ldr
+    int32_t* list = nullptr;       // F : compacted neuron ids (union over samples)
+    uint32_t* bits = nullptr;      // F : per-sample alive bits of each list entry
+    float* list_val = nullptr;     // F x kMaxBatchFast : MC indicator u per entry & sample
+    int* count = nullptr;          // union list length
+    int* done = nullptr;           // last-CTA arrival counter
+    int* alive = nullptr;          // kMaxBatch per-sample alive counts (accumulator)
+    float* ind = nullptr;          // kMaxBatch x F : exact-mode indicator (u or logits)
+    float* ex_s = nullptr;         // kMaxBatch x F : exact-mode s
+    float* ex_lat = nullptr;       // kMaxBatch x ldr : exact-mode latent
+};
+
+struct LaunchCfg {
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool pdl = true;
+};
+
+// Indicator kinds
+enum Method : int { kDense = 0, kMC = 1, kDC = 2 };
+
+// ---------------------------------------------------------------- fast path (UnorderedAccumulate)
+// DC: latent = x theta_a (split over d rows, vector reductions into the zeroed latent).
+cudaError_t launch_latent_fast(const LayerDev& L, const Scratch& S, const float* x, int nb,
+                               const LaunchCfg& c);
+// DC indicator: s_hat = latent theta_bt^T per neuron, threshold s_hat > tau (or override mask),
+// compaction into the union list.  Zeroes y.  Optional mask / logits outputs (B x F).
+cudaError_t launch_indicator_dc_fast(const LayerDev& L, const Scratch& S, int nb, float tau,
+                                     const uint8_t* mask_override, float* y, uint8_t* mask_out,
+                                     float* logits_out, const LaunchCfg& c);
+// MC indicator: u = W_up x per neuron, threshold |u| > tau, compaction (u kept per entry).
+cudaError_t launch_indicator_mc_fast(const LayerDev& L, const Scratch& S, const float* x, int nb,
+                                     float tau, float* y, uint8_t* mask_out, float* u_out,
+                                     const LaunchCfg& c);
+// Fused sparse FFN over the compacted list: gathered up/gate rows (DC) or gate rows (MC,
+// u from the list), act inline, row-sparse W_down accumulate; y += via red.v4.
+// dense=true processes every row (count = F) without a list.
+cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, bool dense,
+                               const float* x, int nb, float* y, int* alive_out,
+                               const LaunchCfg& c);
+// Host-supplied masks (exec_mc / exec_dc): ordered compaction + zero y (+ MC u gather).
+cudaError_t launch_compact_masks(const LayerDev& L, const Scratch& S, const uint8_t* masks,
+                                 const float* u_full, int nb, float* y, const LaunchCfg& c);
+
+// ---------------------------------------------------------------- exact path (DeterministicOrdered)
+// Bitwise-equal to the reference's serial folds (fresh f32 accumulator, ascending index,
+// separate multiply/add roundings, activations in double).
+cudaError_t launch_exact_latent(const LayerDev& L, const Scratch& S, const float* x, int nb,
+                                const LaunchCfg& c);
+// out[b][row] = fold_j W[row][j] * v[b][j] for every row of W (ncols = fold length).
+cudaError_t launch_exact_rowdot_all(const void* W, int dtype, int64_t nrows, int64_t ld,
+                                    int64_t ncols, const float* v, int64_t ldv, int nb,
+                                    float* out, int64_t ldo, const LaunchCfg& c);
+// Ordered union compaction from indicator values (mode 0: |v| > tau, 1: v > tau) or from
+// given masks (mode 2).  Writes masks / per-sample alive counts / list / bits / count.
+cudaError_t launch_exact_compact(const LayerDev& L, const Scratch& S, int mode,
+                                 const float* ind, const uint8_t* masks_in, int nb, float tau,
+                                 uint8_t* mask_out, int* alive_out, const LaunchCfg& c);
+// Phase 1 over the list: DC/dense s = up * act(gate); MC s = act(gate) * u.
+cudaError_t launch_exact_phase1(const LayerDev& L, const Scratch& S, int method,
+                                const float* x, const float* u_full, int nb,
+                                const LaunchCfg& c);
+// y[b][j] = fold over list (ascending neuron) of s * W_down[i][j] for alive samples.
+cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,
+                              const LaunchCfg& c);
+
+// ---------------------------------------------------------------- layout helpers
+cudaError_t launch_pack_rows(const float* src, int64_t rows, int64_t cols, int64_t ld_src,
+                             void* dst, int dtype, int64_t ld_dst, cudaStream_t s);
+// dst (cols_sel x ldr) = transpose of src[:, col_begin:col_begin+cols_sel] (src rows x ld_src).
+cudaError_t launch_pack_transpose(const float* src, int64_t rows, int64_t ld_src,
+                                  int64_t col_begin, int64_t cols_sel, void* dst, int dtype,
+                                  int64_t ld_dst, cudaStream_t s);
+
+}  // namespace cdk

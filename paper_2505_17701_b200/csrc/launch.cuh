@@ -1,0 +1,59 @@
+// launch.cuh -- host-side launch helpers (cudaLaunchKernelEx with optional programmatic
+// dependent launch, dynamic shared-memory opt-in).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "kernels.h"
+
+namespace cdk {
+
+constexpr size_t kMaxDynSmem = 227 * 1024;
+
+// Launch `kernel` on c.stream.  pdl_attr marks the launch as programmatically dependent on
+// the previous kernel in the stream: its CTAs may start while that kernel drains, and must
+// call griddepcontrol.wait before touching anything it produced.
+template <typename K, typename... Args>
+cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, const LaunchCfg& c,
+                      bool pdl_attr, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl_attr && c.pdl) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// Opt the kernel into all the dynamic shared memory it can get (device opt-in limit minus the
+// kernel's static shared memory) once per process; cached, so the per-call host cost is a hash
+// lookup and the call is safe during graph capture.  Fails if `bytes` does not fit.
+template <typename K> cudaError_t set_smem(K kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> limit;
+    std::lock_guard<std::mutex> g(mu);
+    const void* key = reinterpret_cast<const void*>(kernel);
+    auto it = limit.find(key);
+    if (it == limit.end()) {
+        int dev = 0, optin = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa;
+        if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kernel);
+        if (e != cudaSuccess) return e;
+        const size_t lim = static_cast<size_t>(optin) - fa.sharedSizeBytes;
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lim));
+        if (e != cudaSuccess) return e;
+        it = limit.emplace(key, lim).first;
+    }
+    return bytes <= it->second ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+}  // namespace cdk

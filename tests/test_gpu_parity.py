@@ -1,0 +1,359 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on identical inputs.
+
+Contract (BASELINE.json north_star):
+  * DeterministicOrdered ("f32 oracle mode"): masks, indicators and y are BIT-identical to the
+    reference semantics (the oracle is itself pinned bit-for-bit to the reference library).
+  * UnorderedAccumulate (the fused hot path): y within 1e-4 relative L2 of the oracle's
+    forward_sparse on the same mask (f32, and bf16 with the oracle fed the bf16-rounded
+    weights); index sets equal except lanes whose indicator is within a small relative band
+    of the threshold (counted); bf16 vs the original f32 weights within 1e-2.
+  * Dead lanes are never read: NaN-poisoned dead rows / u entries cannot propagate
+    (test_blocked_exec.cpp:101-116, acceptance.cpp:292-351).
+"""
+import numpy as np
+import pytest
+
+import paper_2505_17701_b200 as cd
+from paper_2505_17701_b200 import Reduction
+
+from conftest import bf16_round, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+ORD = cd.BlockConfig(reduction=Reduction.DeterministicOrdered)
+FAST = cd.BlockConfig(reduction=Reduction.UnorderedAccumulate)
+
+SHAPES = [  # (seed, d_model, d_inter, d_rank)
+    (101, 20, 48, 6),
+    (102, 24, 96, 8),
+    (103, 17, 53, 5),      # odd dims: padding + scalar tails
+    (104, 64, 256, 16),
+    (105, 130, 300, 24),
+    (106, 512, 2048, 64),
+]
+
+
+def make_case(oracle, seed, d, F, r, act=0, dtype="f32"):
+    g = oracle.generate(seed, d, F, r)
+    if dtype == "bf16":
+        for k in ("w_up", "w_gate", "w_down", "theta_a", "theta_b"):
+            g[k] = bf16_round(g[k])
+    layer = cd.GatedMlpLayer(d, F, act, g["w_up"], g["w_gate"], g["w_down"], device_dtype=dtype)
+    pred = cd.Predictor(cd.LowRankPredictor(d, r, F, g["theta_a"], g["theta_b"]), dtype)
+    return g, layer, pred
+
+
+def bits_equal(a, b) -> bool:
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def top_m_tau(v, m):
+    v = np.abs(np.asarray(v, np.float32))
+    order = np.lexsort((np.arange(len(v)), -v))
+    return float(v[order[m]])
+
+
+# ----------------------------------------------------------------------------- exact mode
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_exact_dc_pipeline_bitwise(oracle, shape, act, dtype):
+    seed, d, F, r = shape
+    g, layer, pred = make_case(oracle, seed, d, F, r, act, dtype)
+    x = g["x"]
+    for tau_d in (0.0, float(np.median(oracle.lowrank_logits(g["theta_a"], g["theta_b"], x)[1]))):
+        want = oracle.pipeline_dc(g, x, tau_d=tau_d, act=act)
+        got = cd.pipeline_dc(layer, x, pred, ORD, tau_d=tau_d, want_logits=True)
+        assert bits_equal(got.logits, want["logits"])
+        assert np.array_equal(got.mask.alive, want["mask"])
+        assert got.mask.alive_count == want["alive"]
+        assert bits_equal(got.y, want["y"])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_exact_mc_pipeline_bitwise(oracle, shape, act, dtype):
+    seed, d, F, r = shape
+    g, layer, _ = make_case(oracle, seed, d, F, r, act, dtype)
+    x = g["x"]
+    u = oracle.gemv(g["w_up"], x)
+    tau = top_m_tau(u, F // 4)
+    want = oracle.pipeline_mc(g, x, tau, act=act)
+    got = cd.pipeline_mc(layer, x, tau, ORD, want_u=True)
+    assert bits_equal(got.u, want["u"])
+    assert np.array_equal(got.mask.alive, want["mask"])
+    assert got.mask.alive_count == want["alive"]
+    assert bits_equal(got.y, want["y"])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES[:4])
+def test_exact_dense_bitwise(oracle, shape, act, dtype):
+    seed, d, F, r = shape
+    g, layer, _ = make_case(oracle, seed, d, F, r, act, dtype)
+    want = oracle.forward_dense(g, g["x"], act=act)["y"]
+    assert bits_equal(cd.exec_dense(layer, g["x"], ORD), want)
+    # full-mask sparse forward == dense (test_sparsity.cpp:117-127)
+    assert bits_equal(cd.forward_sparse(layer, g["x"], cd.ActivationMask.all_alive(F)), want)
+
+
+@pytest.mark.parametrize("shape", SHAPES[:5])
+def test_exact_exec_never_reads_dead_lanes(oracle, shape):
+    """NaN-poisoned dead rows and u entries (test_blocked_exec.cpp:101-116)."""
+    seed, d, F, r = shape
+    g = oracle.generate(seed, d, F, r)
+    x = g["x"]
+    tr = oracle.forward_dense(g, x)
+    _, mask = oracle.top_m_threshold(tr["s"], max(1, F // 3))
+    want = oracle.forward_sparse(g, x, mask)
+    bad = {k: (v.copy() if v is not None else None) for k, v in g.items()}
+    dead = mask == 0
+    for k in ("w_up", "w_gate", "w_down"):
+        bad[k][dead] = np.nan
+    u_bad = tr["u"].copy()
+    u_bad[dead] = np.nan
+    layer = cd.GatedMlpLayer(d, F, 0, bad["w_up"], bad["w_gate"], bad["w_down"])
+    for red in (ORD, FAST):
+        y_dc = cd.exec_dc(layer, x, mask, red)
+        y_mc = cd.exec_mc(layer, x, u_bad, mask, red)
+        assert np.all(np.isfinite(y_dc)) and np.all(np.isfinite(y_mc))
+        if red is ORD:
+            assert bits_equal(y_dc, want) and bits_equal(y_mc, want)
+        else:
+            assert rel_l2(y_dc, want) <= 1e-4 and rel_l2(y_mc, want) <= 1e-4
+
+
+# ----------------------------------------------------------------------------- fast mode
+def check_mask_flips(got_mask, want_mask, indicator, tau, band):
+    """Index sets equal except lanes within `band` (relative) of the threshold."""
+    diff = np.nonzero(got_mask != want_mask)[0]
+    scale = max(abs(tau), float(np.sqrt(np.mean(np.square(indicator.astype(np.float64))))))
+    dist = np.abs(np.abs(indicator[diff]) - abs(tau)) if tau != 0 else np.abs(indicator[diff] - tau)
+    assert np.all(dist <= band * scale), (diff, dist / scale)
+    return len(diff)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fast_dc_pipeline(oracle, shape, act, dtype):
+    seed, d, F, r = shape
+    g, layer, pred = make_case(oracle, seed, d, F, r, act, dtype)
+    x = g["x"]
+    _, z = oracle.lowrank_logits(g["theta_a"], g["theta_b"], x)
+    for tau_d in (0.0, float(np.quantile(z, 0.8))):
+        got = cd.pipeline_dc(layer, x, pred, FAST, tau_d=tau_d, want_logits=True)
+        assert rel_l2(got.logits, z) <= 1e-5
+        want_mask = (z > tau_d).astype(np.uint8)
+        check_mask_flips(got.mask.alive, want_mask, z, tau_d, 1e-4)
+        assert got.mask.alive_count == int(got.mask.alive.sum())
+        y_ref = oracle.forward_sparse(g, x, got.mask.alive, act=act)
+        assert rel_l2(got.y, y_ref) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fast_mc_pipeline(oracle, shape, act, dtype):
+    seed, d, F, r = shape
+    g, layer, _ = make_case(oracle, seed, d, F, r, act, dtype)
+    x = g["x"]
+    u = oracle.gemv(g["w_up"], x)
+    tau = top_m_tau(u, max(1, F // 3))
+    got = cd.pipeline_mc(layer, x, tau, FAST, want_u=True)
+    assert rel_l2(got.u, u) <= 1e-5
+    check_mask_flips(got.mask.alive, (np.abs(u) > tau).astype(np.uint8), u, tau, 1e-4)
+    y_ref = oracle.forward_sparse(g, x, got.mask.alive, act=act)
+    assert rel_l2(got.y, y_ref) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fast_dense(oracle, shape, dtype):
+    seed, d, F, r = shape
+    g, layer, _ = make_case(oracle, seed, d, F, r, 0, dtype)
+    want = oracle.forward_dense(g, g["x"])["y"]
+    assert rel_l2(cd.exec_dense(layer, g["x"], FAST), want) <= 1e-4
+
+
+def test_fast_unordered_within_tolerance_of_ordered(oracle):
+    """test_blocked_exec.cpp:87-99 on the device: Unordered vs Ordered <= 1e-4."""
+    g, layer, _ = make_case(oracle, 103, 24, 96, 8)
+    tr = oracle.forward_dense(g, g["x"])
+    _, mask = oracle.top_m_threshold(tr["s"], 48)
+    a = cd.exec_dc(layer, g["x"], mask, ORD)
+    b = cd.exec_dc(layer, g["x"], mask, FAST)
+    assert np.linalg.norm(a.astype(np.float64) - b) <= 1e-4 * np.linalg.norm(a.astype(np.float64)) + 1e-12
+
+
+def test_bf16_against_f32_weights_within_1e2(oracle):
+    seed, d, F, r = 106, 512, 2048, 64
+    g = oracle.generate(seed, d, F, r)
+    layer = cd.GatedMlpLayer(d, F, 0, g["w_up"], g["w_gate"], g["w_down"], device_dtype="bf16")
+    pred = cd.Predictor(cd.LowRankPredictor(d, r, F, g["theta_a"], g["theta_b"]), "bf16")
+    got = cd.pipeline_dc(layer, g["x"], pred, FAST)
+    want = oracle.forward_sparse(g, g["x"], got.mask.alive)
+    assert rel_l2(got.y, want) <= 1e-2
+
+
+# ----------------------------------------------------------------------------- batching
+@pytest.mark.parametrize("B", [2, 3, 4, 6, 9])
+@pytest.mark.parametrize("red", ["ord", "fast"])
+def test_batched_per_sample_masks(oracle, B, red):
+    seed, d, F, r = 104, 64, 256, 16
+    g, layer, pred = make_case(oracle, seed, d, F, r)
+    rng = oracle.rng(7)
+    X = np.stack([rng.normals_f(d) for _ in range(B)])
+    cfg = ORD if red == "ord" else FAST
+    res = cd.pipeline_dc(layer, X, pred, cfg, tau_d=0.1)
+    u_all = [oracle.gemv(g["w_up"], X[b]) for b in range(B)]
+    tau_u = float(np.median(np.abs(np.concatenate(u_all))))
+    res_mc = cd.pipeline_mc(layer, X, tau_u, cfg)
+    for b in range(B):
+        want = oracle.pipeline_dc(g, X[b], tau_d=0.1)
+        want_mc = oracle.pipeline_mc(g, X[b], tau_u)
+        if red == "ord":
+            assert bits_equal(res.y[b], want["y"]) and np.array_equal(res.mask[b].alive, want["mask"])
+            assert bits_equal(res_mc.y[b], want_mc["y"]) and np.array_equal(res_mc.mask[b].alive, want_mc["mask"])
+        else:
+            assert rel_l2(res.y[b], oracle.forward_sparse(g, X[b], res.mask[b].alive)) <= 1e-4
+            assert rel_l2(res_mc.y[b], oracle.forward_sparse(g, X[b], res_mc.mask[b].alive)) <= 1e-4
+    yd = cd.exec_dense(layer, X, cfg)
+    for b in range(B):
+        want = oracle.forward_dense(g, X[b])["y"]
+        assert bits_equal(yd[b], want) if red == "ord" else rel_l2(yd[b], want) <= 1e-4
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_empty_and_full_masks(oracle):
+    g, layer, pred = make_case(oracle, 101, 20, 48, 6)
+    x = g["x"]
+    for cfg in (ORD, FAST):
+        assert np.all(cd.exec_dc(layer, x, np.zeros(48, np.uint8), cfg) == 0)
+        assert np.all(cd.pipeline_dc(layer, x, pred, cfg, tau_d=1e30).y == 0)
+        r = cd.pipeline_mc(layer, x, float("inf"), cfg)
+        assert r.mask.alive_count == 0 and np.all(r.y == 0)
+        r = cd.pipeline_mc(layer, x, -1.0, cfg)
+        assert r.mask.alive_count == 48
+    want = oracle.forward_dense(g, x)["y"]
+    assert bits_equal(cd.pipeline_mc(layer, x, -1.0, ORD).y, want)
+
+
+def test_mask_override_keeps_predictor_and_uses_override(oracle):
+    """pipeline_dc(..., mask_override) (blocked_exec.cpp:366-367, test_blocked_exec.cpp:195-212)."""
+    g, layer, pred = make_case(oracle, 109, 20, 48, 4)
+    tr = oracle.forward_dense(g, g["x"])
+    _, ideal = oracle.top_m_threshold(tr["s"], 24)
+    want = oracle.forward_sparse(g, g["x"], ideal)
+    got = cd.pipeline_dc(layer, g["x"], pred, ORD, mask_override=ideal)
+    assert bits_equal(got.y, want) and np.array_equal(got.mask.alive, ideal)
+    got = cd.pipeline_dc(layer, g["x"], pred, FAST, mask_override=ideal)
+    assert rel_l2(got.y, want) <= 1e-4 and np.array_equal(got.mask.alive, ideal)
+    t = cd.traffic_dc_split(cd.ShapeSpec(20, 48, 4, 5, int(ideal.sum())))
+    assert (got.traffic.weight_reads, got.traffic.vector_reads, got.traffic.writes) == (
+        t.weight_reads, t.vector_reads, t.writes)
+
+
+def test_traffic_counters_match_closed_forms(oracle):
+    """test_blocked_exec.cpp:140-175 through the GPU pipelines."""
+    g, layer, pred = make_case(oracle, 107, 16, 64, 6)
+    x = g["x"]
+    u = oracle.gemv(g["w_up"], x)
+    tau_u = top_m_tau(u, 20)
+    for cfg in (ORD, FAST):
+        mc = cd.pipeline_mc(layer, x, tau_u, cfg)
+        want = oracle.traffic_split("mc", 16, 64, 0, mc.mask.alive_count)
+        assert (mc.traffic.weight_reads, mc.traffic.vector_reads, mc.traffic.writes) == want
+        dc = cd.pipeline_dc(layer, x, pred, cfg)
+        want = oracle.traffic_split("dc", 16, 64, 6, dc.mask.alive_count)
+        assert (dc.traffic.weight_reads, dc.traffic.vector_reads, dc.traffic.writes) == want
+        dn = cd.pipeline_dense(layer, x, cfg)
+        assert (dn.traffic.weight_reads, dn.traffic.vector_reads, dn.traffic.writes) == \
+            oracle.traffic_split("dense", 16, 64)
+
+
+def test_predict_logits_and_mask_bitwise(oracle):
+    """predictor.cpp:128-148, incl. the hand example test_predictor.cpp:60-70."""
+    p = cd.Predictor(cd.LowRankPredictor(1, 1, 2, np.array([[2.0]], np.float32),
+                                         np.array([[3.0, -1.0]], np.float32)))
+    z = cd.predict_logits(p, np.array([1.0], np.float32))
+    assert z.tolist() == [6.0, -2.0]
+    m = cd.predict_mask(p, np.array([1.0], np.float32))
+    assert m.alive.tolist() == [1, 0] and m.alive_count == 1 and m.tau == 0.0
+    g = oracle.generate(5, 96, 300, 24)
+    p = cd.Predictor(cd.LowRankPredictor(96, 24, 300, g["theta_a"], g["theta_b"]))
+    assert bits_equal(cd.predict_logits(p, g["x"]), oracle.lowrank_logits(g["theta_a"], g["theta_b"], g["x"])[1])
+
+
+def test_errors_follow_reference_taxonomy(oracle):
+    g, layer, pred = make_case(oracle, 110, 20, 48, 4)
+    with pytest.raises(cd.DataError):
+        cd.exec_dc(layer, g["x"], np.ones(47, np.uint8))
+    with pytest.raises(cd.DataError):
+        cd.exec_dc(layer, g["x"][:-1], np.ones(48, np.uint8))
+    wrong = cd.Predictor(cd.LowRankPredictor(21, 4, 48, np.zeros((21, 4), np.float32),
+                                             np.zeros((4, 48), np.float32)))
+    with pytest.raises(cd.DataError):
+        cd.pipeline_dc(layer, g["x"], wrong)
+    with pytest.raises(cd.DataError):
+        cd.forward_practical(layer, g["x"], cd.SparsityConfig(cd.SparsityMethod.MCountdown,
+                                                               cd.SparsityMode.Practical, 0.5),
+                             cd.PracticalContext())
+
+
+def test_forward_practical_hand_layers():
+    """test_sparsity.cpp:165-233 on the device."""
+    up = np.array([[1.0], [2.0]], np.float32)
+    gate = np.array([[3.0], [-1.0]], np.float32)
+    down = np.array([[1.0], [1.0]], np.float32)
+    layer = cd.GatedMlpLayer(1, 2, cd.Activation.Silu, up, gate, down)
+    x = np.array([1.0], np.float32)
+    mc = cd.forward_practical(layer, x, cd.SparsityConfig(cd.SparsityMethod.MCountdown,
+                                                          cd.SparsityMode.Practical, 0.5),
+                              cd.PracticalContext(tau_hat=1.5))
+    assert mc.mask.alive.tolist() == [0, 1]
+    assert mc.y[0] == cd.forward_sparse(layer, x, mc.mask)[0]
+    ones = np.ones((2, 1), np.float32)
+    layer2 = cd.GatedMlpLayer(1, 2, cd.Activation.Silu, ones, ones, ones)
+    p = cd.Predictor(cd.LowRankPredictor(1, 1, 2, np.array([[1.0]], np.float32),
+                                         np.array([[1.0, -1.0]], np.float32)))
+    dc = cd.forward_practical(layer2, x, cd.SparsityConfig(cd.SparsityMethod.DCountdown,
+                                                           cd.SparsityMode.Practical, 0.5),
+                              cd.PracticalContext(predictor=p))
+    assert dc.mask.alive.tolist() == [1, 0]
+
+
+def test_blocking_knobs_do_not_change_bits(oracle):
+    """acceptance.cpp:336-342: blk_m x blk_n grid is bit-invariant."""
+    g, layer, pred = make_case(oracle, 4321, 29, 70, 5, 1)
+    tr = oracle.forward_dense(g, g["x"], act=1)
+    _, mask = oracle.top_m_threshold(tr["s"], 70 // 3)
+    outs = [cd.exec_dc(layer, g["x"], mask, cd.BlockConfig(bm, bn, Reduction.DeterministicOrdered))
+            for bm in (1, 3, 8) for bn in (1, 4)]
+    assert all(bits_equal(o, outs[0]) for o in outs)
+
+
+def test_device_forward_graph_capture(oracle):
+    """The device-pointer entry point is capturable in a CUDA graph and replays correctly."""
+    import torch
+    seed, d, F, r = 106, 512, 2048, 64
+    g, layer, pred = make_case(oracle, seed, d, F, r, 0, "bf16")
+    dev = layer.device_layer(pred)
+    x = torch.from_numpy(g["x"]).cuda()
+    y = torch.empty(d, device="cuda")
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    dev.forward_device(2, x, y, tau=0.0, stream=s.cuda_stream)  # warm (smem attrs)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph, stream=s):
+        dev.forward_device(2, x, y, tau=0.0, stream=torch.cuda.current_stream().cuda_stream)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    _, z = oracle.lowrank_logits(g["theta_a"], g["theta_b"], g["x"])
+    want = oracle.forward_sparse(g, g["x"], (z > 0).astype(np.uint8))
+    assert rel_l2(y.cpu().numpy(), want) <= 1e-4

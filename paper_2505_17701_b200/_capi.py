@@ -12,7 +12,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libcountdown_b200.so")
+LIB_PATH = os.path.join(HERE, os.environ.get("CD_LIB_DIR", "_lib"), "libcountdown_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "countdown_b200.h")
 
 CD_OK, CD_ERR_USAGE, CD_ERR_DATA, CD_ERR_NUMERIC, CD_ERR_CUDA = 0, 1, 2, 3, 4

@@ -110,11 +110,11 @@ using cdk::kMaxBatchFast;
 // Upload rows [row_begin, row_end) of a full host matrix (rows x cols f32) into a padded
 // device matrix (dtype, row stride ld), via an f32 staging buffer and the pack kernel.
 void upload_rows(cd_layer* h, const float* host, int64_t row_begin, int64_t nrows, int64_t cols,
-                 void* dst, int64_t ld, float* tmp) {
+                 void* dst, int64_t ld_pad, int64_t ld_dst, float* tmp) {
     ck(cudaMemcpyAsync(tmp, host + row_begin * cols, sizeof(float) * nrows * cols,
                        cudaMemcpyHostToDevice, h->stream),
        "upload");
-    ck(cdk::launch_pack_rows(tmp, nrows, cols, cols, dst, h->L.dtype, ld, h->stream), "pack_rows");
+    ck(cdk::launch_pack_rows(tmp, nrows, cols, cols, dst, h->L.dtype, ld_pad, ld_dst, h->stream), "pack_rows");
 }
 
 struct Req {
@@ -196,7 +196,7 @@ int run_chain(cd_layer* h, const Req& r) {
             ck(cdk::launch_exact_compact(L, S, 3, nullptr, nullptr, n, 0.0f, mo, ao, c), "compact");
             launches += 1;
         } else if (r.method == cdk::kMC) {
-            ck(cdk::launch_exact_rowdot_all(L.w_up, L.dtype, F, L.ld, d, xc, d, n, ind, F, c), "rowdot_up");
+            ck(cdk::launch_exact_rowdot_all(L.w_up, L.dtype, F, L.rs, d, xc, d, n, ind, F, c), "rowdot_up");
             ck(cdk::launch_exact_compact(L, S, 0, ind, nullptr, n, r.tau, mo, ao, c), "compact");
             u_full = ind;
             launches += 2;
@@ -325,22 +325,25 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     L.d = d;
     L.F = re - rb;
     L.ld = round_up(d, cdk::kVecElems);
+    L.rs = 3 * L.ld;
     L.act = act;
     L.dtype = dtype;
     h->F_total = F_total;
     h->row_begin = rb;
     const size_t esz = dtype == CD_DTYPE_BF16 ? 2 : 4;
-    const size_t nw = static_cast<size_t>(L.F * L.ld);
+    const size_t nw = static_cast<size_t>(L.F * L.rs);
     if (!predictor_only) {
-    void* wu = h->dalloc<uint8_t>(nw * esz, false);
-    void* wg = h->dalloc<uint8_t>(nw * esz, false);
-    void* wd = h->dalloc<uint8_t>(nw * esz, false);
+    // neuron records [up | gate | down]; the padding columns are zeroed by the pack kernel
+    uint8_t* rec = h->dalloc<uint8_t>(nw * esz, false);
+    void* wu = rec;
+    void* wg = rec + L.ld * esz;
+    void* wd = rec + 2 * L.ld * esz;
     float* tmp = nullptr;
     ck(cudaMalloc(&tmp, sizeof(float) * L.F * d), "cudaMalloc tmp");
     try {
-        upload_rows(h.get(), w_up, rb, L.F, d, wu, L.ld, tmp);
-        upload_rows(h.get(), w_gate, rb, L.F, d, wg, L.ld, tmp);
-        upload_rows(h.get(), w_down, rb, L.F, d, wd, L.ld, tmp);
+        upload_rows(h.get(), w_up, rb, L.F, d, wu, L.ld, L.rs, tmp);
+        upload_rows(h.get(), w_gate, rb, L.F, d, wg, L.ld, L.rs, tmp);
+        upload_rows(h.get(), w_down, rb, L.F, d, wd, L.ld, L.rs, tmp);
         ck(cudaStreamSynchronize(h->stream), "upload");
     } catch (...) {
         cudaFree(tmp);
@@ -429,7 +432,7 @@ int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, co
         const size_t tmp_n = static_cast<size_t>(std::max(L.d * d_rank, d_rank * h->F_total));
         ck(cudaMalloc(&tmp, sizeof(float) * tmp_n), "cudaMalloc tmp");
         cudaError_t e = cudaMemcpyAsync(tmp, theta_a, sizeof(float) * L.d * d_rank, cudaMemcpyHostToDevice, h->stream);
-        if (e == cudaSuccess) e = cdk::launch_pack_rows(tmp, L.d, d_rank, d_rank, ta, L.dtype, ldr, h->stream);
+        if (e == cudaSuccess) e = cdk::launch_pack_rows(tmp, L.d, d_rank, d_rank, ta, L.dtype, ldr, ldr, h->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(tmp, theta_b, sizeof(float) * d_rank * h->F_total, cudaMemcpyHostToDevice, h->stream);
@@ -672,6 +675,15 @@ int cd_bench_device(cd_layer* h, int method, int64_t batch, const float* x, floa
         ck(err, "bench");
     });
 }
+
+#ifdef CD_TIMELINE
+CD_API int cd_debug_timeline(unsigned long long* out, int64_t n) {
+    return guarded([&] {
+        ck(cudaDeviceSynchronize(), "sync");
+        ck(cdk::read_timeline(out, n), "timeline");
+    });
+}
+#endif
 
 int cd_layer_sync(cd_layer* h) {
     return guarded([&] {

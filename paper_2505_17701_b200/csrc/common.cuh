@@ -71,6 +71,45 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// Transpose ("halving") reduction of V partial sums held by every lane (V a power of 2, <= 32):
+// each step exchanges half the remaining values with the partner lane, so V sums cost
+// (V-1) + log2(32/V) shuffles instead of 5V.  Returns the full warp sum of value
+// index transpose_idx<V>(lane); the 32/V lanes of a group hold the same value.
+template <int V>
+__device__ __forceinline__ float warp_transpose_sum(float (&v)[V]) {
+    static_assert(V >= 1 && V <= 32 && (V & (V - 1)) == 0, "V must be a power of two <= 32");
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int h = V / 2, o = 16; h >= 1; h /= 2, o /= 2) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const float send = upper ? v[i] : v[i + h];
+            const float keep = upper ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    float r = v[0];
+#pragma unroll
+    for (int o = 16 / V; o >= 1; o /= 2) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r;
+}
+
+template <int V> __device__ __forceinline__ int transpose_idx(int lane) { return lane / (32 / V); }
+
+// Blackwell packed FP32 FMA (FFMA2): (a0, a1) += (b0, b1) * (c0, c1), two lanes of work per
+// instruction.
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float b0, float b1, float c0, float c1) {
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+        "mov.b64 ra, {%0, %1};\n\t"
+        "mov.b64 rb, {%2, %3};\n\t"
+        "mov.b64 rc, {%4, %5};\n\t"
+        "fma.rn.f32x2 ra, rb, rc, ra;\n\t"
+        "mov.b64 {%0, %1}, ra;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+
 // ---------------------------------------------------------------- global reductions
 // red.global.add.v4.f32 (sm_90+): one vector reduction instead of four scalar atomics.
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -165,5 +204,21 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+
+// ---------------------------------------------------------------- timeline probe
+// Compiled in only with -DCD_TIMELINE (the _lib_tl/ development build): per-CTA
+// %globaltimer stamps at kernel phases, read back with cd_debug_timeline().
+constexpr int kTlKernels = 8, kTlCtas = 160, kTlPhases = 8;
+#ifdef CD_TIMELINE
+static __device__ unsigned long long g_timeline[kTlKernels][kTlCtas][kTlPhases];
+__device__ __forceinline__ void tl_stamp(int kernel, int phase) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < kTlCtas) g_timeline[kernel][blockIdx.x][phase] = t;
+}
+#define TL(k, p) ::cdk::tl_stamp((k), (p))
+#else
+#define TL(k, p) ((void)0)
+#endif
 
 }  // namespace cdk

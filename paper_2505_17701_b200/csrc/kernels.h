@@ -1,9 +1,15 @@
 // kernels.h -- host-side launch interface of the COUNTDOWN sm_100a kernels.
 //
 // Device data layout (one layer / one tensor-parallel shard), all in HBM:
-//   w_up, w_gate, w_down : F x ld, neuron-major row-major (gated_mlp.hpp:16-19 layout), ld =
-//                          round_up(d, 8) zero-padded so every row is a whole number of
-//                          16-byte vectors -> one contiguous run per neuron for the TMA engine.
+//   neuron records       : F x [up | gate | down], each part ld = round_up(d, 8) elements
+//                          (zero-padded to whole 16-byte vectors).  The reference stores the
+//                          three matrices neuron-major (gated_mlp.hpp:16-19); here the three
+//                          rows of one neuron are also adjacent, so an active neuron is ONE
+//                          contiguous run of 3*ld elements = one TMA bulk copy (a bulk copy
+//                          costs ~170 ns of per-SM issue time regardless of size, so three
+//                          separate 8 KB row copies cap an SM at ~28 GB/s -- measured).
+//                          w_up / w_gate / w_down point into the record (offsets 0, ld, 2ld)
+//                          with row stride rs = 3*ld.
 //   theta_a              : d x ldr (reference layout, predictor.hpp:17), ldr = round_up(r, 8).
 //   theta_bt             : F x ldr, theta_b (r x F, predictor.hpp:18) transposed so one
 //                          neuron's predictor row is contiguous.
@@ -21,7 +27,8 @@ constexpr int kMaxBatchFast = 4;   // samples per fused-kernel instance (union o
 constexpr int kMaxBatch = 32;      // samples per call (bitmask width)
 
 struct LayerDev {
-    int64_t d = 0, F = 0, ld = 0;  // d_model, rows in this shard, padded row stride
+    int64_t d = 0, F = 0, ld = 0;  // d_model, rows in this shard, padded row length
+    int64_t rs = 0;                // stride between consecutive neurons' rows (= 3*ld)
     int act = 0, dtype = 0;
     const void* w_up = nullptr;
     const void* w_gate = nullptr;
@@ -100,9 +107,13 @@ cudaError_t launch_exact_phase1(const LayerDev& L, const Scratch& S, int method,
 cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,
                               const LaunchCfg& c);
 
+// Development build only (-DCD_TIMELINE): copy the per-CTA phase stamps to the host.
+cudaError_t read_timeline(unsigned long long* out, int64_t n);
+
 // ---------------------------------------------------------------- layout helpers
+// dst row r = src row r (cols values, zero-padded to ld_pad), rows ld_dst apart.
 cudaError_t launch_pack_rows(const float* src, int64_t rows, int64_t cols, int64_t ld_src,
-                             void* dst, int dtype, int64_t ld_dst, cudaStream_t s);
+                             void* dst, int dtype, int64_t ld_pad, int64_t ld_dst, cudaStream_t s);
 // dst (cols_sel x ldr) = transpose of src[:, col_begin:col_begin+cols_sel] (src rows x ld_src).
 cudaError_t launch_pack_transpose(const float* src, int64_t rows, int64_t ld_src,
                                   int64_t col_begin, int64_t cols_sel, void* dst, int dtype,

@@ -153,14 +153,14 @@ __global__ void ke_phase1(LayerDev L, Scratch S, int method, const float* __rest
     float s = 0.0f;
     if ((bits >> b) & 1u) {
         const int64_t i = S.list[slot];
-        const W* wg = static_cast<const W*>(L.w_gate) + i * L.ld;
+        const W* wg = static_cast<const W*>(L.w_gate) + i * L.rs;
         const float* xb = x + b * L.d;
         if (method == kMC) {
             float g = 0.0f;
             for (int64_t j = 0; j < L.d; ++j) g = __fadd_rn(g, __fmul_rn(ldw(wg + j), xb[j]));
             s = __fmul_rn(act_exact(L.act, g), u_full[b * L.F + i]);
         } else {
-            const W* wu = static_cast<const W*>(L.w_up) + i * L.ld;
+            const W* wu = static_cast<const W*>(L.w_up) + i * L.rs;
             float u = 0.0f, g = 0.0f;
             for (int64_t j = 0; j < L.d; ++j) {
                 u = __fadd_rn(u, __fmul_rn(ldw(wu + j), xb[j]));
@@ -186,7 +186,7 @@ __global__ void ke_down(LayerDev L, Scratch S, float* __restrict__ y) {
     float acc = 0.0f;
     for (int slot = 0; slot < n; ++slot) {
         if (!((S.bits[slot] >> b) & 1u)) continue;
-        acc = __fadd_rn(acc, __fmul_rn(sb[slot], ldw(WD + (int64_t)S.list[slot] * L.ld + j)));
+        acc = __fadd_rn(acc, __fmul_rn(sb[slot], ldw(WD + (int64_t)S.list[slot] * L.rs + j)));
     }
     y[b * L.d + j] = acc;
 }
@@ -200,12 +200,12 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
 
 template <typename W>
 __global__ void k_pack_rows(const float* __restrict__ src, int64_t rows, int64_t cols,
-                            int64_t ld_src, W* __restrict__ dst, int64_t ld_dst) {
-    const int64_t n = rows * ld_dst;
+                            int64_t ld_src, W* __restrict__ dst, int64_t ld_pad, int64_t ld_dst) {
+    const int64_t n = rows * ld_pad;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / ld_dst, c = e % ld_dst;
-        dst[e] = from_f32<W>(c < cols ? src[r * ld_src + c] : 0.0f);
+        const int64_t r = e / ld_pad, c = e % ld_pad;
+        dst[r * ld_dst + c] = from_f32<W>(c < cols ? src[r * ld_src + c] : 0.0f);
     }
 }
 
@@ -279,13 +279,14 @@ cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float
 }
 
 cudaError_t launch_pack_rows(const float* src, int64_t rows, int64_t cols, int64_t ld_src,
-                             void* dst, int dtype, int64_t ld_dst, cudaStream_t s) {
-    const int blocks = static_cast<int>(imin64(4096, (rows * ld_dst + 255) / 256));
+                             void* dst, int dtype, int64_t ld_pad, int64_t ld_dst, cudaStream_t s) {
+    const int blocks = static_cast<int>(imin64(4096, (rows * ld_pad + 255) / 256));
     if (dtype == kBF16)
         k_pack_rows<__nv_bfloat16><<<blocks, 256, 0, s>>>(src, rows, cols, ld_src,
-                                                          static_cast<__nv_bfloat16*>(dst), ld_dst);
+                                                          static_cast<__nv_bfloat16*>(dst), ld_pad, ld_dst);
     else
-        k_pack_rows<float><<<blocks, 256, 0, s>>>(src, rows, cols, ld_src, static_cast<float*>(dst), ld_dst);
+        k_pack_rows<float><<<blocks, 256, 0, s>>>(src, rows, cols, ld_src, static_cast<float*>(dst), ld_pad,
+                                                  ld_dst);
     return cudaGetLastError();
 }
 

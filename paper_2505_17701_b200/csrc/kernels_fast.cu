@@ -42,6 +42,7 @@ template <typename W, int NB>
 __global__ void __launch_bounds__(256) k_latent_fast(LayerDev L, const float* __restrict__ x,
                                                      float* __restrict__ latent,
                                                      int rows_per_cta) {
+    if (threadIdx.x == 0) TL(0, 0);
     pdl_launch_dependents();
     __shared__ float red[NB * 2048];
     const int nvr = static_cast<int>(L.ldr / kVec);
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(256) k_latent_fast(LayerDev L, const float* __
             red_add_v4(latent + b * L.ldr + c * 4, s[0], s[1], s[2], s[3]);
         }
     }
+    if (threadIdx.x == 0) TL(0, 1);
 }
 
 // ============================================================================ DC indicator
@@ -95,6 +97,7 @@ __global__ void k_indicator_dc(LayerDev L, Scratch S, int nb, int rows_per_cta, 
                                int nstages, float tau, const uint8_t* __restrict__ ovr,
                                float* __restrict__ y, int64_t y_len, uint8_t* __restrict__ mask_out,
                                float* __restrict__ logits_out) {
+    if (threadIdx.x == 0) TL(1, 0);
     pdl_launch_dependents();
     extern __shared__ __align__(1024) uint8_t smem[];
     const int nwc = blockDim.x / kWarp - 1;  // consumer warps
@@ -107,6 +110,8 @@ __global__ void k_indicator_dc(LayerDev L, Scratch S, int nb, int rows_per_cta, 
     uint32_t* l_bits = reinterpret_cast<uint32_t*>(l_idx + rows_per_cta);
     int* n_local = reinterpret_cast<int*>(l_bits + rows_per_cta);
     int* alive_local = n_local + 1;
+    float* wscratch = reinterpret_cast<float*>(alive_local + kMaxBatchFast);  // [nwc][kRB*NB]
+    constexpr int kRB = 4;
 
     const int64_t c0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t c1 = imin64(L.F, c0 + rows_per_cta);
@@ -147,60 +152,92 @@ __global__ void k_indicator_dc(LayerDev L, Scratch S, int nb, int rows_per_cta, 
         }
     } else {
         // ---- consumers: one warp per predictor row, latent held in registers.
+        if (threadIdx.x == 0) TL(1, 1);
         pdl_wait();
+        if (threadIdx.x == 0) TL(1, 2);
         const int nvr = static_cast<int>(L.ldr / kVec);
         float lat[NB][VPL][8];
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
             const int vec = lane + v * kWarp;
 #pragma unroll
-            for (int b = 0; b < NB; ++b)
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    lat[b][v][k] = (vec < nvr && b < nb) ? __ldcg(S.latent + b * L.ldr + vec * kVec + k) : 0.0f;
+            for (int b = 0; b < NB; ++b) {
+                float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+                if (vec < nvr && b < nb) {
+                    const float4* src = reinterpret_cast<const float4*>(S.latent + b * L.ldr + vec * kVec);
+                    lo = __ldcg(src);
+                    hi = __ldcg(src + 1);
+                }
+                lat[b][v][0] = lo.x; lat[b][v][1] = lo.y; lat[b][v][2] = lo.z; lat[b][v][3] = lo.w;
+                lat[b][v][4] = hi.x; lat[b][v][5] = hi.y; lat[b][v][6] = hi.z; lat[b][v][7] = hi.w;
+            }
         }
+        if (threadIdx.x == 0) TL(1, 3);
+        // Each warp takes kRB consecutive rows at a time: packed FFMA2 dot products, one
+        // halving (transpose) shuffle reduction for all kRB x NB sums, then lanes 0..kRB-1
+        // own one row each for thresholding and ballot compaction (one shared atomic per
+        // kRB rows).
         int st = 0;
         uint32_t ph = 0;
         for (int s = 0; s < nst; ++s) {
             const int64_t r0 = c0 + (int64_t)s * stage_rows;
             const int n = static_cast<int>(imin64(stage_rows, c1 - r0));
             mbar_wait(&full[st], ph);
+            if (threadIdx.x == 0 && s == 0) TL(1, 4);
             const W* base = reinterpret_cast<const W*>(smem + st * stage_bytes);
-            for (int rr = warp; rr < n; rr += nwc) {
-                float acc[NB];
+            for (int rr0 = warp * kRB; rr0 < n; rr0 += nwc * kRB) {
+                constexpr int kV = kRB * NB;
+                float v[kV];
 #pragma unroll
-                for (int b = 0; b < NB; ++b) acc[b] = 0.0f;
+                for (int j = 0; j < kRB; ++j) {
+                    float w[VPL][8];
 #pragma unroll
-                for (int v = 0; v < VPL; ++v) {
-                    const int vec = lane + v * kWarp;
-                    if (vec < nvr) {
-                        float w[8];
-                        Vec8<W>::load(base + rr * L.ldr + vec * kVec, w);
+                    for (int q = 0; q < VPL; ++q) {
+                        const int vec = lane + q * kWarp;
+                        if (rr0 + j < n && vec < nvr) Vec8<W>::load(base + (rr0 + j) * L.ldr + vec * kVec, w[q]);
+                        else
 #pragma unroll
-                        for (int b = 0; b < NB; ++b)
-#pragma unroll
-                            for (int k = 0; k < 8; ++k) acc[b] = fmaf(w[k], lat[b][v][k], acc[b]);
+                            for (int k = 0; k < 8; ++k) w[q][k] = 0.0f;
                     }
-                }
-#pragma unroll
-                for (int b = 0; b < NB; ++b) acc[b] = warp_sum(acc[b]);
-                if (lane == 0) {
-                    const int64_t gi = r0 + rr;
-                    uint32_t bits = 0;
 #pragma unroll
                     for (int b = 0; b < NB; ++b) {
-                        if (b >= nb) break;
-                        const bool a = ovr ? (ovr[b * L.F + gi] != 0) : (acc[b] > tau);
-                        bits |= static_cast<uint32_t>(a) << b;
+                        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+                        for (int q = 0; q < VPL; ++q)
+#pragma unroll
+                            for (int k = 0; k < 8; k += 2) ffma2(a0, a1, w[q][k], w[q][k + 1], lat[b][q][k], lat[b][q][k + 1]);
+                        v[j * NB + b] = a0 + a1;
+                    }
+                }
+                const float tot = warp_transpose_sum<kV>(v);
+                // lanes g*(32/kV) hold value index g = row j * NB + sample b
+                if ((lane % (32 / kV)) == 0) wscratch[warp * kV + lane / (32 / kV)] = tot;
+                __syncwarp();
+                const bool valid = lane < kRB && rr0 + lane < n;
+                const int64_t gi = r0 + rr0 + lane;
+                uint32_t bits = 0;
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    bool a = false;
+                    if (valid && b < nb) {
+                        const float z = wscratch[warp * kV + lane * NB + b];
+                        a = ovr ? (ovr[b * L.F + gi] != 0) : (z > tau);
                         if (mask_out) mask_out[b * L.F + gi] = a ? 1 : 0;
-                        if (logits_out) logits_out[b * L.F + gi] = acc[b];
-                        if (a) atomicAdd(&alive_local[b], 1);
+                        if (logits_out) logits_out[b * L.F + gi] = z;
                     }
-                    if (bits) {
-                        const int e = atomicAdd(n_local, 1);
-                        l_idx[e] = static_cast<int32_t>(gi);
-                        l_bits[e] = bits;
-                    }
+                    bits |= static_cast<uint32_t>(a) << b;
+                    const unsigned bal = __ballot_sync(0xffffffffu, a);
+                    if (lane == 0 && bal) atomicAdd(&alive_local[b], __popc(bal));
+                }
+                __syncwarp();
+                const unsigned any = __ballot_sync(0xffffffffu, bits != 0);
+                int e0 = 0;
+                if (lane == 0 && any) e0 = atomicAdd(n_local, __popc(any));
+                e0 = __shfl_sync(0xffffffffu, e0, 0);
+                if (bits) {
+                    const int e = e0 + __popc(any & ((1u << lane) - 1u));
+                    l_idx[e] = static_cast<int32_t>(gi);
+                    l_bits[e] = bits;
                 }
             }
             __syncwarp();
@@ -208,6 +245,7 @@ __global__ void k_indicator_dc(LayerDev L, Scratch S, int nb, int rows_per_cta, 
             if (++st == nstages) { st = 0; ph ^= 1; }
         }
     }
+    if (threadIdx.x == 0) TL(1, 5);
     __syncthreads();
     __shared__ int base_s;
     if (threadIdx.x == 0) {
@@ -220,6 +258,7 @@ __global__ void k_indicator_dc(LayerDev L, Scratch S, int nb, int rows_per_cta, 
         S.list[base_s + e] = l_idx[e];
         S.bits[base_s + e] = l_bits[e];
     }
+    if (threadIdx.x == 0) TL(1, 6);
 }
 
 // ============================================================================ MC indicator
@@ -232,6 +271,7 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
                                int rows_per_cta, int nstages, float tau, float* __restrict__ y,
                                int64_t y_len, uint8_t* __restrict__ mask_out,
                                float* __restrict__ u_out) {
+    if (threadIdx.x == 0) TL(4, 0);
     pdl_launch_dependents();
     extern __shared__ __align__(1024) uint8_t smem[];
     const int nwc = blockDim.x / kWarp - 1;
@@ -242,7 +282,7 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
     const int64_t stage_bytes = row_bytes * kSR;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + stage_bytes * nstages);
     uint64_t* empty = full + nstages;
-    float* red = reinterpret_cast<float*>(empty + nstages);  // [2][nwc][kSR*NB]
+    float* red = reinterpret_cast<float*>(empty + nstages);  // [2][nwc][kSR*NB] partial sums
     int32_t* l_idx = reinterpret_cast<int32_t*>(red + 2 * nwc * kSR * NB);
     uint32_t* l_bits = reinterpret_cast<uint32_t*>(l_idx + rows_per_cta);
     float* l_val = reinterpret_cast<float*>(l_bits + rows_per_cta);  // [rows_per_cta][NB]
@@ -279,8 +319,9 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
                 const int n = static_cast<int>(imin64(kSR, c1 - r0));
                 mbar_wait(&empty[st], ph ^ 1);
                 mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(n * row_bytes));
-                bulk_g2s(smem + st * stage_bytes, U + r0 * L.ld, static_cast<uint32_t>(n * row_bytes),
-                         &full[st], pol);
+                for (int q = 0; q < n; ++q)
+                    bulk_g2s(smem + st * stage_bytes + q * row_bytes, U + (r0 + q) * L.rs,
+                             static_cast<uint32_t>(row_bytes), &full[st], pol);
                 if (++st == nstages) { st = 0; ph ^= 1; }
             }
         }
@@ -305,11 +346,13 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
             const int n = static_cast<int>(imin64(kSR, c1 - r0));
             mbar_wait(&full[st], ph);
             const W* base = reinterpret_cast<const W*>(smem + st * stage_bytes);
-            float p[kSR][NB];
+            constexpr int kV = kSR * NB;
+            float v[kV];
 #pragma unroll
             for (int rr = 0; rr < kSR; ++rr) {
+                float a0[NB], a1[NB];
 #pragma unroll
-                for (int b = 0; b < NB; ++b) p[rr][b] = 0.0f;
+                for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0f;
                 if (rr < n) {
 #pragma unroll
                     for (int j = 0; j < VPT; ++j) {
@@ -320,41 +363,46 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
 #pragma unroll
                             for (int b = 0; b < NB; ++b)
 #pragma unroll
-                                for (int k = 0; k < 8; ++k) p[rr][b] = fmaf(w[k], xr[b][j][k], p[rr][b]);
+                                for (int k = 0; k < 8; k += 2) ffma2(a0[b], a1[b], w[k], w[k + 1], xr[b][j][k], xr[b][j][k + 1]);
                         }
                     }
                 }
+#pragma unroll
+                for (int b = 0; b < NB; ++b) v[rr * NB + b] = a0[b] + a1[b];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);  // stage data consumed
-            float* rb = red + (s & 1) * nwc * kSR * NB;
-#pragma unroll
-            for (int rr = 0; rr < kSR; ++rr)
-#pragma unroll
-                for (int b = 0; b < NB; ++b) {
-                    const float v = warp_sum(p[rr][b]);
-                    if (lane == 0) rb[(warp * kSR + rr) * NB + b] = v;
-                }
+            const float tot = warp_transpose_sum<kV>(v);
+            float* rb = red + (s & 1) * nwc * kV;
+            if ((lane % (32 / kV)) == 0) rb[warp * kV + lane / (32 / kV)] = tot;
             named_bar_sync(1, nc);
-            if (ct < n) {
-                const int rr = ct;
-                const int64_t gi = r0 + rr;
+            if (warp == 0) {
+                const bool valid = lane < n;
+                const int64_t gi = r0 + lane;
                 uint32_t bits = 0;
                 float uv[NB];
 #pragma unroll
                 for (int b = 0; b < NB; ++b) {
                     float u = 0.0f;
-                    for (int w = 0; w < nwc; ++w) u += rb[(w * kSR + rr) * NB + b];
+                    if (valid)
+                        for (int w = 0; w < nwc; ++w) u += rb[w * kV + lane * NB + b];
                     uv[b] = u;
-                    if (b >= nb) continue;
-                    const bool a = fabsf(u) > tau;
+                    bool a = false;
+                    if (valid && b < nb) {
+                        a = fabsf(u) > tau;
+                        if (mask_out) mask_out[b * L.F + gi] = a ? 1 : 0;
+                        if (u_out) u_out[b * L.F + gi] = u;
+                    }
                     bits |= static_cast<uint32_t>(a) << b;
-                    if (mask_out) mask_out[b * L.F + gi] = a ? 1 : 0;
-                    if (u_out) u_out[b * L.F + gi] = u;
-                    if (a) atomicAdd(&alive_local[b], 1);
+                    const unsigned bal = __ballot_sync(0xffffffffu, a);
+                    if (lane == 0 && bal) atomicAdd(&alive_local[b], __popc(bal));
                 }
+                const unsigned any = __ballot_sync(0xffffffffu, bits != 0);
+                int e0 = 0;
+                if (lane == 0 && any) e0 = atomicAdd(n_local, __popc(any));
+                e0 = __shfl_sync(0xffffffffu, e0, 0);
                 if (bits) {
-                    const int e = atomicAdd(n_local, 1);
+                    const int e = e0 + __popc(any & ((1u << lane) - 1u));
                     l_idx[e] = static_cast<int32_t>(gi);
                     l_bits[e] = bits;
 #pragma unroll
@@ -378,6 +426,7 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
 #pragma unroll
         for (int b = 0; b < NB; ++b) S.list_val[(int64_t)(base_s + e) * kMaxBatchFast + b] = l_val[e * NB + b];
     }
+    if (threadIdx.x == 0) TL(4, 6);
 }
 
 // ============================================================================ sparse FFN
@@ -385,6 +434,8 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
 // warp bulk-copies the neuron's (up,) gate and down rows -- each one contiguous run -- into a
 // ring stage; consumers (column owners) reduce the dot products across the CTA, apply the
 // activation and accumulate s * W_down[i] into register-resident y.
+constexpr int kGroup = 4;  // neurons per reduction round in k_sparse
+
 struct SlotMeta {
     int32_t idx;
     uint32_t bits;
@@ -394,6 +445,8 @@ struct SlotMeta {
 template <typename W, int NB, int VPT, bool kMC>
 __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict__ x, int nstages,
                          bool dense, float* __restrict__ y, int* __restrict__ alive_out) {
+    constexpr int kTl = kMC ? 3 : 2;
+    if (threadIdx.x == 0) TL(kTl, 0);
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int kRows = kMC ? 2 : 3;  // rows per neuron: (up,) gate, down
     const int nwc = blockDim.x / kWarp - 1;
@@ -405,7 +458,8 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + stage_bytes * nstages);
     uint64_t* empty = full + nstages;
     SlotMeta* meta = reinterpret_cast<SlotMeta*>(empty + nstages);
-    float* red = reinterpret_cast<float*>(meta + nstages);  // [2][nwc][2*NB]
+    float* red = reinterpret_cast<float*>(meta + nstages);  // [nwc][kGroup * 2 * NB] warp sums
+    float* sval = red + nwc * kGroup * 2 * NB;                // [kGroup * NB] activations s
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < nstages; ++s) {
@@ -417,6 +471,7 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
     __syncthreads();
 
     pdl_wait();  // list / count / y-zeroing of the upstream kernel are now visible
+    if (threadIdx.x == 0) TL(kTl, 1);
     const int n = dense ? static_cast<int>(L.F) : __ldcg(S.count);
     const int G = gridDim.x;
     if (!kMC && !dense && blockIdx.x == 0) {
@@ -469,10 +524,8 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
                     for (int b = 0; b < NB; ++b) meta[st].u[b] = u[b];
                     uint8_t* dst = smem + st * stage_bytes;
                     mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(kRows * row_bytes));
-                    int m = 0;
-                    if (!kMC) bulk_g2s(dst + (m++) * row_bytes, WU + (int64_t)i * L.ld, (uint32_t)row_bytes, &full[st], pol);
-                    bulk_g2s(dst + (m++) * row_bytes, WG + (int64_t)i * L.ld, (uint32_t)row_bytes, &full[st], pol);
-                    bulk_g2s(dst + (m++) * row_bytes, WD + (int64_t)i * L.ld, (uint32_t)row_bytes, &full[st], pol);
+                    // one bulk copy per neuron: its record part [(up,) gate, down] is contiguous
+                    bulk_g2s(dst, (kMC ? WG : WU) + (int64_t)i * L.rs, (uint32_t)(kRows * row_bytes), &full[st], pol);
                 }
                 __syncwarp();
                 if (++st == nstages) { st = 0; ph ^= 1; }
@@ -495,78 +548,102 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
                     yr[b][j][k] = 0.0f;
                 }
         }
+        // Slots are consumed kGroup at a time: packed-FFMA2 partial dot products of up to
+        // kGroup neurons, ONE halving shuffle reduction for all of them, one named barrier;
+        // warp 0 alone finishes the cross-warp sums and the activation (no redundant work in
+        // the other warps), a second barrier publishes s, then every column owner
+        // accumulates s * W_down[i] into its register-resident y with FFMA2.
+        constexpr int kM = kMC ? 1 : 2;            // gate (, up) sums per neuron
+        constexpr int kV = kGroup * kM * NB;       // partial sums per lane per group
         int st = 0;
         uint32_t ph = 0;
         int it = 0;
-        for (int slot = blockIdx.x; slot < n; slot += G, ++it) {
-            mbar_wait(&full[st], ph);
-            const uint8_t* sbase = smem + st * stage_bytes;
-            const W* rup = reinterpret_cast<const W*>(sbase);
-            const W* rgate = reinterpret_cast<const W*>(sbase + (kMC ? 0 : row_bytes));
-            const W* rdown = reinterpret_cast<const W*>(sbase + (kMC ? 1 : 2) * row_bytes);
-            float pu[NB], pg[NB];
+        for (int base = blockIdx.x; base < n; base += G * kGroup, ++it) {
+            const int ns = min(kGroup, (n - base + G - 1) / G);
+            int sts[kGroup];
+            float v[kV];
 #pragma unroll
-            for (int b = 0; b < NB; ++b) pu[b] = pg[b] = 0.0f;
+            for (int q = 0; q < kGroup; ++q) {
+                sts[q] = st;
+                float g0[NB], g1[NB], u0[NB], u1[NB];
 #pragma unroll
-            for (int j = 0; j < VPT; ++j) {
-                const int vec = ct + j * nc;
-                if (vec < nvec) {
-                    float wg[8];
-                    Vec8<W>::load(rgate + vec * kVec, wg);
+                for (int b = 0; b < NB; ++b) g0[b] = g1[b] = u0[b] = u1[b] = 0.0f;
+                if (q < ns) {
+                    mbar_wait(&full[st], ph);
+                    if (threadIdx.x == 0 && it == 0 && q == 0) TL(kTl, 2);
+                    const uint8_t* sbase = smem + st * stage_bytes;
+                    const W* rup = reinterpret_cast<const W*>(sbase);
+                    const W* rgate = reinterpret_cast<const W*>(sbase + (kMC ? 0 : row_bytes));
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)
+                    for (int j = 0; j < VPT; ++j) {
+                        const int vec = ct + j * nc;
+                        if (vec < nvec) {
+                            float wg[8], wu[8];
+                            Vec8<W>::load(rgate + vec * kVec, wg);
+                            if (!kMC) Vec8<W>::load(rup + vec * kVec, wu);
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) pg[b] = fmaf(wg[k], xr[b][j][k], pg[b]);
-                    if (!kMC) {
-                        float wu[8];
-                        Vec8<W>::load(rup + vec * kVec, wu);
+                            for (int b = 0; b < NB; ++b)
 #pragma unroll
-                        for (int b = 0; b < NB; ++b)
-#pragma unroll
-                            for (int k = 0; k < 8; ++k) pu[b] = fmaf(wu[k], xr[b][j][k], pu[b]);
+                                for (int k = 0; k < 8; k += 2) {
+                                    ffma2(g0[b], g1[b], wg[k], wg[k + 1], xr[b][j][k], xr[b][j][k + 1]);
+                                    if (!kMC) ffma2(u0[b], u1[b], wu[k], wu[k + 1], xr[b][j][k], xr[b][j][k + 1]);
+                                }
+                        }
                     }
+                    if (++st == nstages) { st = 0; ph ^= 1; }
                 }
-            }
-            float* rb = red + (it & 1) * nwc * 2 * NB;
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                const float g = warp_sum(pg[b]);
-                const float u = kMC ? 0.0f : warp_sum(pu[b]);
-                if (lane == 0) {
-                    rb[(warp * 2) * NB + b] = g;
-                    rb[(warp * 2 + 1) * NB + b] = u;
+                for (int b = 0; b < NB; ++b) {
+                    v[(q * kM) * NB + b] = g0[b] + g1[b];
+                    if (!kMC) v[(q * kM + 1) * NB + b] = u0[b] + u1[b];
                 }
             }
+            const float tot = warp_transpose_sum<kV>(v);
+            if ((lane % (32 / kV)) == 0) red[warp * kV + lane / (32 / kV)] = tot;
             named_bar_sync(1, nc);
-            const uint32_t bits = meta[st].bits;
-            float sv[NB];
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
+            if (warp == 0 && lane < ns * NB) {
+                const int q = lane / NB, b = lane % NB;
                 float g = 0.0f, u = 0.0f;
                 for (int w = 0; w < nwc; ++w) {
-                    g += rb[(w * 2) * NB + b];
-                    u += rb[(w * 2 + 1) * NB + b];
+                    g += red[w * kV + (q * kM) * NB + b];
+                    if (!kMC) u += red[w * kV + (q * kM + 1) * NB + b];
                 }
-                if (kMC) u = meta[st].u[b];
-                sv[b] = ((bits >> b) & 1u) ? (kMC ? act_fast(L.act, g) * u : u * act_fast(L.act, g)) : 0.0f;
+                int sq = sts[0];
+#pragma unroll
+                for (int qq = 1; qq < kGroup; ++qq) sq = (q == qq) ? sts[qq] : sq;
+                if (kMC) u = meta[sq].u[b];
+                const bool alive = (meta[sq].bits >> b) & 1u;
+                sval[lane] = alive ? (kMC ? act_fast(L.act, g) * u : u * act_fast(L.act, g)) : 0.0f;
             }
+            named_bar_sync(1, nc);
 #pragma unroll
-            for (int j = 0; j < VPT; ++j) {
-                const int vec = ct + j * nc;
-                if (vec < nvec) {
-                    float wd[8];
-                    Vec8<W>::load(rdown + vec * kVec, wd);
+            for (int q = 0; q < kGroup; ++q) {
+                if (q < ns) {
+                    const int sq = sts[q];
+                    float sv[NB];
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)
+                    for (int b = 0; b < NB; ++b) sv[b] = sval[q * NB + b];
+                    const W* rdown = reinterpret_cast<const W*>(smem + sq * stage_bytes + (kMC ? 1 : 2) * row_bytes);
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) yr[b][j][k] = fmaf(sv[b], wd[k], yr[b][j][k]);
+                    for (int j = 0; j < VPT; ++j) {
+                        const int vec = ct + j * nc;
+                        if (vec < nvec) {
+                            float wd[8];
+                            Vec8<W>::load(rdown + vec * kVec, wd);
+#pragma unroll
+                            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                                for (int k = 0; k < 8; k += 2)
+                                    ffma2(yr[b][j][k], yr[b][j][k + 1], sv[b], sv[b], wd[k], wd[k + 1]);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[sq]);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            if (++st == nstages) { st = 0; ph ^= 1; }
         }
         // ---- one vector reduction per owned column group
+        if (threadIdx.x == 0) TL(kTl, 3);
         if (n > blockIdx.x) {
 #pragma unroll
             for (int j = 0; j < VPT; ++j) {
@@ -595,7 +672,9 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
     // ---- last CTA restores the self-cleaning scratch (count, done, alive accumulators).
     __syncthreads();
     if (threadIdx.x == 0) {
+        TL(kTl, 4);
         __threadfence();
+        TL(kTl, 5);
         const int prev = atomicAdd(S.done, 1);
         if (prev == G - 1) {
             __threadfence();
@@ -606,6 +685,7 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
             atomicExch(S.count, 0);
             atomicExch(S.done, 0);
         }
+        TL(kTl, 6);
     }
 }
 
@@ -622,6 +702,19 @@ int consumer_warps(int64_t nvec, int vpt) {
 }
 
 }  // namespace
+
+#ifdef CD_TIMELINE
+cudaError_t read_timeline(unsigned long long* out, int64_t n) {
+    const size_t cnt = (size_t)kTlKernels * kTlCtas * kTlPhases;
+    if ((size_t)n < cnt) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_timeline, cnt * sizeof(unsigned long long));
+    static unsigned long long zeros[kTlKernels * kTlCtas * kTlPhases];
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_timeline, zeros, sizeof(zeros));
+    return e;
+}
+#else
+cudaError_t read_timeline(unsigned long long*, int64_t) { return cudaErrorNotSupported; }
+#endif
 
 // ---------------------------------------------------------------- public launchers
 cudaError_t launch_latent_fast(const LayerDev& L, const Scratch& S, const float* x, int nb,
@@ -655,10 +748,10 @@ cudaError_t launch_indicator_dc_fast(const LayerDev& L, const Scratch& S, int nb
     const int64_t esz = L.dtype == kBF16 ? 2 : 4;
     const int64_t row_bytes = L.ldr * esz;
     const int stage_rows = static_cast<int>(std::max<int64_t>(1, kStageBytesTarget / row_bytes));
-    const int64_t tail = 16 * 16 + (int64_t)rpc * 8 + 64;
+    const int64_t tail = 16 * 16 + (int64_t)rpc * 8 + 64 + 8 * 16 * 4;
     int nstages = static_cast<int>(imin64(8, (kSmemBudget - tail) / (stage_rows * row_bytes)));
     nstages = std::max(nstages, 2);
-    const size_t smem = stage_rows * row_bytes * nstages + 2 * nstages * 8 + (size_t)rpc * 8 + 64;
+    const size_t smem = stage_rows * row_bytes * nstages + 2 * nstages * 8 + (size_t)rpc * 8 + 64 + 8 * 16 * 4;
     const int threads = (8 + 1) * kWarp;
     const int64_t y_len = (int64_t)nb * L.d;
     auto go = [&](auto kern) {
@@ -786,11 +879,11 @@ cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, 
     const bool mc = method == kMC;
     const int64_t esz = L.dtype == kBF16 ? 2 : 4;
     const int64_t stage_bytes = L.ld * esz * (mc ? 2 : 3);
-    const int64_t tail = 2 * 8 * 8 + 8 * (int64_t)sizeof(SlotMeta) + (int64_t)2 * nwc * 2 * nbk * 4 + 64;
+    const int64_t red_bytes = ((int64_t)nwc * kGroup * 2 * nbk + kGroup * nbk) * 4;
+    const int64_t tail = 2 * 8 * 8 + 8 * (int64_t)sizeof(SlotMeta) + red_bytes + 64;
     int nstages = static_cast<int>(imin64(8, (kSmemBudget - tail) / stage_bytes));
     if (nstages < 2) return cudaErrorInvalidValue;
-    const size_t smem = stage_bytes * nstages + 2 * nstages * 8 + nstages * sizeof(SlotMeta) +
-                        (size_t)2 * nwc * 2 * nbk * 4 + 64;
+    const size_t smem = stage_bytes * nstages + 2 * nstages * 8 + nstages * sizeof(SlotMeta) + red_bytes + 64;
     if (dense) {
         // Dense comparator: no indicator kernel upstream, so zero y in a tiny PDL-primary kernel.
         cudaError_t e = launch_ex(k_zero, dim3(64), dim3(256), 0, c, false, y, (int64_t)nb * L.d);

@@ -1,0 +1,452 @@
+"""bench.py -- COUNTDOWN sparse Gated-MLP FFN decode on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the one the metric is quoted on): one Gated-MLP layer of
+Llama-3.1-8B shape (d=4096, d_ff=14336, SiLU), bf16 weights (f32 x / y / accumulation),
+batch-1 decode, D-CountDown (low-rank predictor r=512) at 90% target sparsity.  Weights,
+predictor and inputs are the reference bench()'s seeded synthetic workload
+(blocked_exec.cpp:396-415, bit-identical RNG), RNE-rounded to bf16 on upload.  tau_D is
+calibrated per layer as the mean over 32 calibration inputs of each input's exact top-m
+logit threshold (calibration.cpp:11-37 extended to the predictor logits, Alg. 3
+PAPER.md:645); timed inputs are 16 other N(0,1) vectors.
+
+A "step" = one token through one FFN layer.  `value` = tokens/s of the fused chain with
+inputs resident in HBM: K steps captured in one CUDA graph, rotating over NL layer replicas
+whose touched rows together exceed the 126 MB L2 (so every step streams its rows from HBM),
+timed with CUDA events, barrier + synchronize on both sides, max over ranks.  `e2e` = the
+same metric through the reference-facing C-ABI call with HOST buffers (cd_pipeline_dc:
+H2D of x, the chain, D2H of y and the alive count, synchronous), wall-clock per call.
+
+N > 1 (torchrun): d_ff tensor-parallel over the ranks, NCCL all-reduce of y
+per step inside the graph; strong scaling (the same token stream, split neurons).
+
+`--impl reference`: the reference's own CPU implementation (oracle/_ref, the unmodified
+library built from /root/reference/proj/src) on the host cores: pipeline_dc on the same
+layer / inputs with the same alive sets (mask_override = logits > tau_D computed by the
+reference's predict_logits), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D, F, R = 4096, 14336, 512
+SEED = 42
+N_CAL, N_X = 32, 16
+METRIC = "FFN decode tokens/s + effective HBM GB/s vs sparsity, Llama-3.1-8B shape"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=400)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--k", type=float, default=0.9)
+    p.add_argument("--layers", type=int, default=8, help="layer replicas rotated per step (L2-cold)")
+    p.add_argument("--no-sweep", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- workload
+def workload():
+    """Seeded layer + predictor (reference bench() order), calibration and timed inputs."""
+    import paper_2505_17701_b200 as cd
+    layer, _, pred = cd.synth_workload(SEED, D, F, R, device_dtype="bf16")
+    xcal = np.stack([cd.synth_normals(10_000 + i, D) for i in range(N_CAL)])
+    xs = np.stack([cd.synth_normals(1_000 + i, D) for i in range(N_X)])
+    return layer, pred, xcal, xs
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_baseline_sample():
+    """The reference library's own bench() (blocked_exec.cpp:391-455): DC, Llama shape, k=0.9,
+    Ordered, blk 16/256 (cmd_bench's defaults), all host threads; p50 of a bounded sample."""
+    import oracle as O
+    if not O.reference_available():
+        return None
+    ref = O.Reference()
+    iters = 10
+    t0 = time.time()
+    r = ref.bench("dc", D, F, R, 0.9, iters, seed=SEED)
+    return {"value": 1e9 / r["p50_ns"], "unit": "tokens/s", "cores": ref.max_threads(),
+            "kind": "reference",
+            "sample": f"reference bench(dc, d={D}, d_ff={F}, r={R}, k=0.9, iters={iters}) p50 "
+                      f"{r['p50_ns']/1e6:.2f} ms/token, f32, OpenMP Ordered blk 16/256 "
+                      f"({time.time()-t0:.1f} s incl. setup)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    if not O.reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcountdown_ref.so not built"}))
+        return
+    ref = O.Reference()
+    import paper_2505_17701_b200 as cd  # host-only helpers (synthetic normals), no device use
+    g = ref.generate(SEED, D, F, R)
+    xcal = np.stack([cd.synth_normals(10_000 + i, D) for i in range(N_CAL)])
+    xs = np.stack([cd.synth_normals(1_000 + i, D) for i in range(N_X)])
+    m = cd.alive_count_for(args.k, F)
+    taus = []
+    for x in xcal:
+        z = ref.predict_logits(g["theta_a"], g["theta_b"], x)
+        order = np.lexsort((np.arange(F), -z))
+        taus.append(float(z[order[m]]))
+    tau = float(np.mean(taus))
+    masks = [(ref.predict_logits(g["theta_a"], g["theta_b"], x) > np.float32(tau)).astype(np.uint8) for x in xs]
+    for i in range(args.warmup):
+        ref.pipeline_dc(g, xs[i % N_X], masks[i % N_X])
+    t0 = time.perf_counter()
+    alive = 0
+    for i in range(args.steps):
+        r = ref.pipeline_dc(g, xs[i % N_X], masks[i % N_X])
+        alive += r["alive"]
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    cores = ref.max_threads()
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"llama3.1-8b FFN layer d={D} d_ff={F}, D-CountDown r={R} k={args.k}, batch 1 "
+                                   "decode (reference CPU pipeline_dc, mask_override = logits > tau_D)",
+                       "realized_sparsity": 1 - alive / args.steps / F},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                             "sample": f"{args.steps} tokens x pipeline_dc, OpenMP {cores} threads, Ordered"},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- ours
+def graph_rate(torch, fwd, steps, stream, reps_soak=0):
+    """Capture `steps` decode steps in one CUDA graph; return (ms for one replay, graph)."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            cs = torch.cuda.current_stream().cuda_stream
+            for i in range(steps):
+                fwd(i, cs)
+    g.replay()
+    torch.cuda.synchronize()
+    for _ in range(reps_soak):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), g
+
+
+def run_ours(args):
+    import torch
+    import paper_2505_17701_b200 as cd
+    from paper_2505_17701_b200 import costmodel as cm
+    from paper_2505_17701_b200.tp import TPLayer, allreduce_sum_
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak, peak_kind = peaks()
+
+    layer, pred, xcal, xs = workload()
+    # thresholds: tau_D per k (calibrated with the exact kernels on the full layer's logits)
+    m_of = lambda k: cd.alive_count_for(k, F)
+    z_cal = np.atleast_2d(cd.predict_logits(pred, xcal))
+    z_x = np.atleast_2d(cd.predict_logits(pred, xs))
+
+    def tau_dc(k):
+        m = m_of(k)
+        return float(np.mean([row[np.lexsort((np.arange(F), -row))[m]] for row in z_cal]))
+
+    NL = args.layers
+    tps = [TPLayer(layer, pred, world, rank, device=local, device_dtype="bf16") for _ in range(NL)]
+    devs = [t.dev for t in tps]
+    x_dev = torch.from_numpy(xs).cuda()
+    y_dev = torch.zeros((NL, N_X, D), device="cuda")
+    alive_dev = torch.zeros((NL * N_X,), dtype=torch.int32, device="cuda")
+    stream = torch.cuda.Stream()
+
+    def step_fn(method, tau, comm=True):
+        def f(i, cs):
+            li, xi = i % NL, i % N_X
+            tps[li].forward_local(method, x_dev[xi], y_dev[li, xi], tau, cs)
+            if comm and world > 1:
+                allreduce_sum_(y_dev[li, xi])
+        return f
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    rb, re_ = tps[0].rows
+    Fl = re_ - rb
+
+    def alive_of(tau):
+        return (z_x[:, rb:re_] > np.float32(tau)).sum(axis=1)  # this rank's alive rows per input
+
+    def chain_bytes(method, alive_local):
+        return cm.device_bytes(method, D, Fl, R if method == "dc" else 0, int(alive_local), 2)["total_bytes"]
+
+    # ---- headline: DC at k (default 0.9)
+    tau = tau_dc(args.k)
+    fwd = step_fn(cd._capi.METHOD_DC, tau)
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            fwd(i, stream.cuda_stream)
+    torch.cuda.synchronize()
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+    clk = ClockSampler(int(vis[local]) if len(vis) > local and vis[local].strip().isdigit() else local)
+    with clk:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(g, stream=stream):
+                cs = torch.cuda.current_stream().cuda_stream
+                for i in range(args.steps):
+                    fwd(i, cs)
+        for _ in range(max(3, int(0.6e3 / max(1e-3, 0.012 * args.steps)))):  # ~0.6 s soak
+            g.replay()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+        e1.record(stream)
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+    launches_per_step = devs[0].last_launches()
+    value = args.steps / (ms / 1e3)
+    alive_x = alive_of(tau)
+    alive_full = (z_x > np.float32(tau)).sum(axis=1)
+    realized = 1.0 - float(alive_full.mean()) / F
+    bytes_step = float(np.mean([chain_bytes("dc", a) for a in alive_x]))
+    del g
+
+    # ---- dominant kernel roofline: per-stage device times (PDL off, events between kernels)
+    st_iters = 64
+    stage_ns = cd.DeviceLayer.bench_stages(devs, cd._capi.METHOD_DC, x_dev[0], tau, 8, st_iters)
+    a0 = int(alive_x[0])
+    stage_bytes = [D * R * 2 + 4 * D + 4 * R,          # latent: theta_a + x + latent
+                   Fl * R * 2 + 4 * R + 4 * D,          # indicator: theta_bt + latent (+ y zeroing)
+                   3 * a0 * D * 2 + 4 * D * 2 + 8 * a0]  # sparse: 3 rows per alive neuron + x, y, list
+    names = ["k_latent_fast", "k_indicator_dc", "k_sparse<DC>"]
+    dom = int(np.argmax(stage_ns))
+    achieved = stage_bytes[dom] / stage_ns[dom]  # bytes/ns == GB/s
+    stages = [{"kernel": n, "us": ns / 1e3, "alg_bytes": b, "gbs": b / ns}
+              for n, ns, b in zip(names, stage_ns, stage_bytes)]
+
+    # ---- e2e through the C-ABI with host buffers (rank 0's view; TP adds the all-reduce)
+    e2e = None
+    if world == 1:
+        import ctypes as C
+        from paper_2505_17701_b200._capi import lib, ptr, check
+        L = lib()
+        yh = np.empty(D, np.float32)
+        ah = np.empty(1, np.int64)
+        xs_c = [np.ascontiguousarray(x) for x in xs]
+        for i in range(args.warmup):
+            check(L.cd_pipeline_dc(devs[i % NL].raw, 1, ptr(xs_c[i % N_X]), tau, None, 1, ptr(yh), None, ptr(ah), None))
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            check(L.cd_pipeline_dc(devs[i % NL].raw, 1, ptr(xs_c[i % N_X]), tau, None, 1, ptr(yh), None, ptr(ah), None))
+        dt = time.perf_counter() - t0
+        e2e = {"value": args.steps / dt, "unit": "tokens/s", "h2d_bytes_per_step": 4 * D,
+               "d2h_bytes_per_step": 4 * D + 4, "timing": "wall clock per synchronous C-ABI call",
+               "api": "cd_pipeline_dc (host buffers)"}
+
+    # ---- all-reduce share (TP)
+    comm = None
+    if world > 1:
+        ms_local, gl = graph_rate(torch, step_fn(cd._capi.METHOD_DC, tau, comm=False), args.steps, stream)
+        del gl
+        ms_local = max_over_ranks(ms_local)
+        comm = {"layer_us": 1e3 * ms / args.steps, "compute_only_us": 1e3 * ms_local / args.steps,
+                "allreduce_share": max(0.0, 1 - ms_local / ms), "allreduce_bytes": 4 * D}
+
+    # ---- sparsity sweep (DC 50/70/80/90, MC 70/90, dense 0%)
+    sweep = []
+    if not args.no_sweep:
+        n_sw = min(args.steps, 256)
+        cases = [("dc", k) for k in (0.5, 0.7, 0.8, 0.9)] + [("mc", 0.7), ("mc", 0.9), ("dense", 0.0)]
+        u_cal = u_x = None
+        for method, k in cases:
+            if method == "mc" and u_cal is None:
+                u_cal = np.abs(cd.pipeline_mc(layer, xcal, float("inf"),
+                                              cd.BlockConfig(reduction=cd.Reduction.DeterministicOrdered),
+                                              want_u=True).u)
+                u_x = np.abs(cd.pipeline_mc(layer, xs, float("inf"),
+                                            cd.BlockConfig(reduction=cd.Reduction.DeterministicOrdered),
+                                            want_u=True).u)
+            if method == "dc":
+                t = tau_dc(k)
+                al = (z_x[:, rb:re_] > np.float32(t)).sum(axis=1)
+                alf = (z_x > np.float32(t)).sum(axis=1)
+                mid = cd._capi.METHOD_DC
+            elif method == "mc":
+                m = m_of(k)
+                t = float(np.mean([row[np.lexsort((np.arange(F), -row))[m]] for row in u_cal]))
+                al = (u_x[:, rb:re_] > np.float32(t)).sum(axis=1)
+                alf = (u_x > np.float32(t)).sum(axis=1)
+                mid = cd._capi.METHOD_MC
+            else:
+                t, al, alf, mid = 0.0, np.full(N_X, Fl), np.full(N_X, F), cd._capi.METHOD_DENSE
+            f = step_fn(mid, t)
+            with torch.cuda.stream(stream):
+                for i in range(4):
+                    f(i, stream.cuda_stream)
+            barrier()
+            ms_k, gk = graph_rate(torch, f, n_sw, stream)
+            del gk
+            ms_k = max_over_ranks(ms_k)
+            us = 1e3 * ms_k / n_sw
+            b = float(np.mean([chain_bytes(method, a) for a in al]))
+            sweep.append({"method": method, "k": k, "realized_sparsity": round(1 - float(alf.mean()) / F, 4),
+                          "tokens_per_s": round(1e3 / us * 1e3, 1), "us_per_token": round(us, 3),
+                          "touched_mb_per_rank": round(b / 1e6, 2), "gbs_per_rank": round(b / us / 1e3, 1),
+                          "hbm_frac": round(b / us / 1e3 / peak, 4)})
+        dense = [s for s in sweep if s["method"] == "dense"]
+        dc90 = [s for s in sweep if s["method"] == "dc" and s["k"] == 0.9]
+        if dense and dc90:
+            sweep.append({"speedup_dc90_vs_dense": round(dense[0]["us_per_token"] / dc90[0]["us_per_token"], 2)})
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample()
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (reference bench() seeded RNG, seed 42; bf16-rounded)",
+            "config": {"workload": f"BASELINE configs[1]: llama3.1-8b FFN layer d={D} d_ff={F} SiLU, D-CountDown "
+                                   f"r={R} k={args.k} (tau_D calibrated), batch-1 decode, bf16 weights",
+                       "global_batch": 1, "parallelism": f"tp{world} (d_ff)" if world > 1 else "single",
+                       "realized_sparsity": round(realized, 4),
+                       "l2": f"inputs larger than L2: {NL} layer replicas rotated per step "
+                             f"({NL * bytes_step / 1e6:.0f} MB touched per rotation > 126 MB L2)",
+                       "graph": f"{args.steps} steps in one CUDA graph ({launches_per_step} PDL-chained kernels "
+                                "per step" + (" + NCCL all-reduce" if world > 1 else "") + ")"},
+            "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": None, "alg_bytes_per_launch": stage_bytes[dom],
+                         "stages": stages,
+                         "step": {"alg_bytes": bytes_step, "gbs": round(bytes_step / (1e6 * ms / args.steps), 1),
+                                  "frac": round(bytes_step / (1e6 * ms / args.steps) / peak, 4)}},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "sweep": sweep,
+        }
+        if comm:
+            line["allreduce"] = comm
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

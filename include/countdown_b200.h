@@ -57,10 +57,11 @@ extern "C" {
 #define CD_REDUCTION_ORDERED 0
 #define CD_REDUCTION_UNORDERED 1
 
-/* Method selector for cd_forward_device (costmodel.hpp:52 CostMethod, minus CATS). */
+/* Method selector for cd_forward_device (costmodel.hpp:52 CostMethod). */
 #define CD_METHOD_DENSE 0
 #define CD_METHOD_MC 1
 #define CD_METHOD_DC 2
+#define CD_METHOD_CATS 3
 
 #if defined(__GNUC__)
 #define CD_API __attribute__((visibility("default")))
@@ -122,6 +123,17 @@ CD_API int cd_exec_mc(cd_layer* h, int64_t batch, const float* x, const float* u
 CD_API int cd_exec_dc(cd_layer* h, int64_t batch, const float* x, const uint8_t* mask, int reduction,
                float* y);
 
+/* exec_cats (blocked_exec.hpp:43-44): masked up GEMV times the caller's act(gate)
+ * (batch x d_inter, only alive lanes read), masked down.  CATS is the paper's comparison
+ * baseline, not the COUNTDOWN hot path. */
+CD_API int cd_exec_cats(cd_layer* h, int64_t batch, const float* x, const float* act_gate,
+                        const uint8_t* mask, int reduction, float* y);
+
+/* pipeline_cats (blocked_exec.hpp:63-64): h = act(W_gate x), mask = |h| > tau (strict),
+ * exec_cats.  act_out: batch x d_inter (optional). */
+CD_API int cd_pipeline_cats(cd_layer* h, int64_t batch, const float* x, float tau, int reduction,
+                            float* y, uint8_t* mask_out, int64_t* alive_out, float* act_out);
+
 /* pipeline_mc (blocked_exec.hpp:60-61) / forward_practical MC (sparsity.hpp:53-54):
  * u = W_up x (dense indicator), mask = |u| > tau (strict), sparse gate/down.
  * alive: per-sample alive counts (batch entries); u_out: batch x d_inter. */
@@ -167,6 +179,18 @@ CD_API int cd_predictor_create(int device, int64_t d_model, int64_t d_rank, int6
  * handle's stream; ns_out[i] receives iteration i's device time in nanoseconds. */
 CD_API int cd_bench_device(cd_layer* h, int method, int64_t batch, const float* x, float tau,
                            int reduction, int64_t warmup, int64_t iters, int64_t* ns_out);
+
+/* Per-kernel device time of the fused chain (UnorderedAccumulate, batch <= 4): the chain runs
+ * `warmup + iters` times, rotating over the n_handles layers (so a layer's rows are evicted
+ * from L2 between its uses when the handles together exceed L2), with programmatic dependent
+ * launch OFF and a CUDA event after every kernel.  stage_ns_out[k] receives the SUM over the
+ * timed iterations of stage k's time; *n_stages_out the number of stages (DC 3: latent,
+ * indicator, sparse FFN; MC 2: indicator, sparse FFN; dense 1).  d_x: batch x d_model device
+ * f32.  Used for the roofline of the dominant kernel; the bench's headline rate is timed
+ * with the chain PDL-overlapped (cd_forward_device in a CUDA graph). */
+CD_API int cd_bench_stages(cd_layer* const* hs, int n_handles, int method, int64_t batch,
+                           const float* d_x, float tau, int64_t warmup, int64_t iters,
+                           int64_t* stage_ns_out, int* n_stages_out);
 
 /* ---------------------------------------------------------------- synthetic inputs
  * The reference bench()'s seeded workload (blocked_exec.cpp:396-415): make_random_layer

@@ -19,7 +19,7 @@ CD_OK, CD_ERR_USAGE, CD_ERR_DATA, CD_ERR_NUMERIC, CD_ERR_CUDA = 0, 1, 2, 3, 4
 ACT_SILU, ACT_GELU_TANH = 0, 1
 DTYPE_F32, DTYPE_BF16 = 0, 1
 REDUCTION_ORDERED, REDUCTION_UNORDERED = 0, 1
-METHOD_DENSE, METHOD_MC, METHOD_DC = 0, 1, 2
+METHOD_DENSE, METHOD_MC, METHOD_DC, METHOD_CATS = 0, 1, 2, 3
 
 
 class DataError(RuntimeError):
@@ -56,12 +56,15 @@ _SIGNATURES = {
     "cd_exec_mc": [_vp, _i64, _vp, _vp, _vp, _i32, _vp],
     "cd_exec_dc": [_vp, _i64, _vp, _vp, _i32, _vp],
     "cd_pipeline_mc": [_vp, _i64, _vp, _f32, _i32, _vp, _vp, _vp, _vp],
+    "cd_exec_cats": [_vp, _i64, _vp, _vp, _vp, _i32, _vp],
+    "cd_pipeline_cats": [_vp, _i64, _vp, _f32, _i32, _vp, _vp, _vp, _vp],
     "cd_pipeline_dc": [_vp, _i64, _vp, _f32, _vp, _i32, _vp, _vp, _vp, _vp],
     "cd_predict_logits": [_vp, _i64, _vp, _vp],
     "cd_forward_device": [_vp, _i32, _i64, _vp, _f32, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "cd_layer_sync": [_vp],
     "cd_predictor_create": [_i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp],
     "cd_bench_device": [_vp, _i32, _i64, _vp, _f32, _i32, _i64, _i64, _vp],
+    "cd_bench_stages": [_vp, _i32, _i32, _i64, _vp, _f32, _i64, _i64, _vp, _vp],
     "cd_synth_layer": [_u64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp],
     "cd_synth_normals": [_u64, _i64, _vp],
 }

@@ -36,9 +36,9 @@ __all__ = [
     "Activation", "Reduction", "BlockConfig", "TrafficCounter", "ActivationMask",
     "GatedMlpLayer", "LowRankPredictor", "Predictor", "PredictorKind", "SparsityMethod",
     "SparsityMode", "SparsityConfig", "PracticalContext", "PracticalResult", "PipelineResult",
-    "BenchStats", "DeviceLayer", "exec_dense", "exec_mc", "exec_dc", "pipeline_dense",
-    "pipeline_mc", "pipeline_dc", "forward_sparse", "forward_practical", "predict_logits",
-    "predict_mask", "realized_sparsity", "bench", "synth_workload", "synth_normals",
+    "BenchStats", "DeviceLayer", "exec_dense", "exec_mc", "exec_cats", "exec_dc", "pipeline_dense",
+    "pipeline_mc", "pipeline_cats", "pipeline_dc", "forward_sparse", "forward_practical", "predict_logits",
+    "predict_mask", "calibrate", "realized_sparsity", "bench", "synth_workload", "synth_normals",
     "DataError", "NumericError", "CudaError",
 ]
 
@@ -290,6 +290,24 @@ class DeviceLayer:
         check(lib().cd_exec_dc(self.raw, x.shape[0], ptr(x), ptr(m), int(reduction), ptr(y)))
         return y
 
+    def exec_cats(self, x, act_gate, masks, reduction) -> np.ndarray:
+        x, h = _f32(x), _f32(act_gate)
+        m = np.ascontiguousarray(masks, np.uint8)
+        y = np.empty_like(x)
+        check(lib().cd_exec_cats(self.raw, x.shape[0], ptr(x), ptr(h), ptr(m), int(reduction), ptr(y)))
+        return y
+
+    def pipeline_cats(self, x, tau, reduction, want_act=False):
+        x = _f32(x)
+        B = x.shape[0]
+        y = np.empty_like(x)
+        mask = np.empty((B, self.d_inter), np.uint8)
+        alive = np.empty(B, np.int64)
+        h = np.empty((B, self.d_inter), np.float32) if want_act else None
+        check(lib().cd_pipeline_cats(self.raw, B, ptr(x), float(tau), int(reduction), ptr(y), ptr(mask),
+                                     ptr(alive), ptr(h)))
+        return y, mask, alive, h
+
     def pipeline_mc(self, x, tau, reduction, want_u=False):
         x = _f32(x)
         B = x.shape[0]
@@ -338,6 +356,18 @@ class DeviceLayer:
 
     def sync(self) -> None:
         check(lib().cd_layer_sync(self.raw))
+
+    @staticmethod
+    def bench_stages(layers: "list[DeviceLayer]", method: int, x_dev, tau: float, warmup: int,
+                     iters: int, batch: int = 1) -> list[float]:
+        """Mean device ns of each kernel of the fused chain (PDL off, events between launches),
+        rotating over `layers` so their rows fall out of L2 between uses."""
+        arr = (C.c_void_p * len(layers))(*[l.raw for l in layers])
+        ns = np.zeros(8, np.int64)
+        n = C.c_int()
+        check(lib().cd_bench_stages(arr, len(layers), int(method), int(batch), ptr(x_dev), float(tau),
+                                    int(warmup), int(iters), ptr(ns), C.byref(n)))
+        return [float(v) / iters for v in ns[: n.value]]
 
 
 class GatedMlpLayer:
@@ -469,6 +499,23 @@ def exec_mc(layer: GatedMlpLayer, x, u, mask, cfg: BlockConfig | None = None,
     return y[0] if single else y
 
 
+def exec_cats(layer: GatedMlpLayer, x, act_gate, mask, cfg: BlockConfig | None = None,
+              tc: TrafficCounter | None = None) -> np.ndarray:
+    """exec_cats (blocked_exec.hpp:43-44, blocked_exec.cpp:214-250): masked up GEMV times
+    the caller's act(gate); dead lanes' rows and act_gate entries are never read."""
+    layer.validate()
+    xb, single = _batched(x, layer.d_model, "exec_cats")
+    B, F = xb.shape[0], layer.d_inter
+    masks = _mask_rows(mask, B, F, "exec_cats")
+    hb = np.asarray(act_gate, np.float32)
+    hb = hb.reshape(B, -1) if hb.ndim > 1 or B == 1 else np.tile(hb, (B, 1))
+    if hb.shape[1] != F:
+        raise DataError("exec_cats: act_gate length does not match d_inter")
+    y = layer.device_layer().exec_cats(xb, np.ascontiguousarray(hb), masks, _reduction(cfg))
+    _count_exec(tc, layer.d_model, F, masks.sum(axis=1), "mc")  # same streams as exec_mc
+    return y[0] if single else y
+
+
 def exec_dc(layer: GatedMlpLayer, x, mask, cfg: BlockConfig | None = None,
             tc: TrafficCounter | None = None) -> np.ndarray:
     """exec_dc (blocked_exec.hpp:47-48, blocked_exec.cpp:252-289)."""
@@ -503,6 +550,25 @@ def pipeline_mc(layer: GatedMlpLayer, x, tau: float, cfg: BlockConfig | None = N
     res = PipelineResult(y[0] if single else y, _masks_out(m, alive, tau, single), tc)
     if want_u:
         res.u = u[0] if single else u
+    return res
+
+
+def pipeline_cats(layer: GatedMlpLayer, x, tau: float, cfg: BlockConfig | None = None,
+                  want_act: bool = False) -> PipelineResult:
+    """pipeline_cats (blocked_exec.cpp:330-348): dense gate pass, act, |act| > tau, exec_cats."""
+    layer.validate()
+    xb, single = _batched(x, layer.d_model, "pipeline_cats")
+    d, F = layer.d_model, layer.d_inter
+    y, m, alive, h = layer.device_layer().pipeline_cats(xb, tau, _reduction(cfg), want_act)
+    tc = TrafficCounter()
+    for _ in alive:
+        tc.add(d * F, d, F)          # dense gate pass (blocked_exec.cpp:336-337)
+        tc.add(0, F, F)              # act (:338-342)
+        tc.add(0, 2 * F, 2 * F)      # threshold_mask (:304-310)
+    _count_exec(tc, d, F, alive, "mc")
+    res = PipelineResult(y[0] if single else y, _masks_out(m, alive, tau, single), tc)
+    if want_act:
+        res.act = h[0] if single else h
     return res
 
 
@@ -578,7 +644,38 @@ def forward_practical(layer: GatedMlpLayer, x, cfg: SparsityConfig, ctx: Practic
         return PracticalResult(r.y, r.mask)
     if ctx.tau_hat is None:
         raise DataError("forward_practical: cats needs a calibrated tau_hat")
-    raise DataError("forward_practical: cats is not part of the B200 hot path (SURVEY.md 8f row 3)")
+    r = pipeline_cats(layer, x, float(np.float32(ctx.tau_hat)), bc)
+    return PracticalResult(r.y, r.mask)
+
+
+def calibrate(layer: GatedMlpLayer, xs, k: float, method: SparsityMethod,
+              predictor: Predictor | None = None) -> float:
+    """calibrate (calibration.cpp:11-37) on the device: tau = mean over the T samples of each
+    sample's exact top-m threshold, m = alive_count_for(k, d_inter), accumulated in double
+    in sample order.  MC thresholds |u| (u = W_up x, the exact kernels: bitwise the
+    reference's gemv); DC extends it to the predictor logits s_hat (signed, Alg. 3's tau_D,
+    PAPER.md:645), for which the reference has no calibrator (predict_mask fixes 0)."""
+    xb, _ = _batched(xs, layer.d_model, "calibrate")
+    if xb.shape[0] == 0:
+        raise DataError("calibrate: need at least one sample")
+    m = alive_count_for(k, layer.d_inter)
+    if method == SparsityMethod.MCountdown:
+        ind = np.abs(pipeline_mc(layer, xb, float("inf"), BlockConfig(reduction=Reduction.DeterministicOrdered),
+                                 want_u=True).u)
+    elif method == SparsityMethod.DCountdown:
+        if predictor is None:
+            raise DataError("calibrate: dc needs a predictor")
+        ind = np.atleast_2d(predict_logits(predictor, xb))
+    else:
+        raise DataError("calibrate: cats is not part of the B200 hot path")
+    ind = np.atleast_2d(ind)
+    F = layer.d_inter
+    acc = 0.0
+    for row in ind:
+        # top_m_threshold (numerics.cpp:105-142): the (m+1)-th largest value, ties -> lower index
+        order = np.lexsort((np.arange(F), -row))
+        acc += float(row[order[m]]) if m < F else float("-inf")
+    return acc / ind.shape[0]
 
 
 def realized_sparsity(mask: ActivationMask) -> float:
@@ -615,7 +712,8 @@ def synth_normals(seed: int, n: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- bench
-_METHOD_IDS = {"dense": _capi.METHOD_DENSE, "mc": _capi.METHOD_MC, "dc": _capi.METHOD_DC}
+_METHOD_IDS = {"dense": _capi.METHOD_DENSE, "mc": _capi.METHOD_MC, "dc": _capi.METHOD_DC,
+               "cats": _capi.METHOD_CATS}
 
 
 def bench(method: str, shape: ShapeSpec, k: float, iters: int, cfg: BlockConfig | None = None,
@@ -627,7 +725,7 @@ def bench(method: str, shape: ShapeSpec, k: float, iters: int, cfg: BlockConfig 
     if iters <= 0:
         raise DataError("bench: iters must be positive")
     if method not in _METHOD_IDS:
-        raise DataError(f"unknown method '{method}' (expected dense|mc|dc)")
+        raise DataError(f"unknown method '{method}' (expected dense|cats|mc|dc)")
     d, F = shape.d_model, shape.d_inter
     layer, x, pred = synth_workload(seed, d, F, shape.d_rank if method == "dc" else 0,
                                     device_dtype=device_dtype)
@@ -642,6 +740,10 @@ def bench(method: str, shape: ShapeSpec, k: float, iters: int, cfg: BlockConfig 
             u = np.abs(pipeline_mc(layer, x, float("inf"),
                                    BlockConfig(reduction=Reduction.DeterministicOrdered), want_u=True).u)
             ind = u
+        elif method == "cats":
+            # tau_h = (m+1)-th largest |act(gate)| (blocked_exec.cpp:410)
+            ind = np.abs(pipeline_cats(layer, x, float("inf"),
+                                       BlockConfig(reduction=Reduction.DeterministicOrdered), want_act=True).act)
         else:
             # exact-count DC mask: threshold the predictor's own logits at their (m+1)-th
             # largest value, so exactly m rows are alive (the reference instead overrides
@@ -657,6 +759,8 @@ def bench(method: str, shape: ShapeSpec, k: float, iters: int, cfg: BlockConfig 
         tc = pipeline_dense(layer, x, cfg).traffic
     elif method == "mc":
         tc = pipeline_mc(layer, x, tau, cfg).traffic
+    elif method == "cats":
+        tc = pipeline_cats(layer, x, tau, cfg).traffic
     else:
         tc = pipeline_dc(layer, x, pred, cfg, tau_d=tau).traffic
     dense_total = traffic_dense_split(ShapeSpec(d, F)).total()

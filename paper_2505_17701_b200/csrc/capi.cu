@@ -132,6 +132,8 @@ struct Req {
     float* ind_out = nullptr;
     int* alive_out = nullptr;
     cudaStream_t stream = nullptr;
+    // Stage timing (cd_bench_stages): PDL off, an event recorded after every launch.
+    cudaEvent_t* marks = nullptr;
 };
 
 // Enqueue one operator call (device pointers) on r.stream.  Returns the number of launches.
@@ -143,6 +145,15 @@ int run_chain(cd_layer* h, const Req& r) {
     c.stream = r.stream ? r.stream : h->stream;
     const int64_t d = L.d, F = L.F;
     int launches = 0;
+    if (r.marks) {
+        c.pdl = false;
+        if (r.nb > kMaxBatchFast || r.reduction != CD_REDUCTION_UNORDERED || r.with_masks)
+            fail(CD_ERR_DATA, "stage timing covers the fused chain at batch <= 4 only");
+    }
+    // after each launch of the fused chain: stage-boundary event (timing runs only)
+    auto mark = [&](int n_launched) {
+        if (r.marks) ck(cudaEventRecord(r.marks[n_launched], c.stream), "event");
+    };
     if (r.method == cdk::kDC && !r.with_masks && !L.theta_bt)
         fail(CD_ERR_DATA, "pipeline_dc: layer has no low-rank predictor attached");
     if (!L.w_up) fail(CD_ERR_DATA, "forward: handle holds only a predictor (no layer weights)");
@@ -157,22 +168,30 @@ int run_chain(cd_layer* h, const Req& r) {
             int* ao = r.alive_out ? r.alive_out + c0 : nullptr;
             if (r.with_masks) {
                 ck(cdk::launch_compact_masks(L, S, r.masks_in + c0 * F,
-                                             r.method == cdk::kMC ? r.u_in + c0 * F : nullptr, n, yc, c),
+                                             r.method != cdk::kDC ? r.u_in + c0 * F : nullptr, n, yc, c),
                    "compact_masks");
                 ck(cdk::launch_sparse_fast(L, S, r.method, false, xc, n, yc, ao, c), "sparse");
                 launches += 2;
             } else if (r.method == cdk::kDense) {
+                // two launches: the y-zeroing kernel, then the all-rows FFN kernel
                 ck(cdk::launch_sparse_fast(L, S, cdk::kDC, true, xc, n, yc, ao, c), "dense");
                 launches += 2;
-            } else if (r.method == cdk::kMC) {
-                ck(cdk::launch_indicator_mc_fast(L, S, xc, n, r.tau, yc, mo, io, c), "indicator_mc");
-                ck(cdk::launch_sparse_fast(L, S, cdk::kMC, false, xc, n, yc, ao, c), "sparse_mc");
+                mark(0);
+            } else if (r.method == cdk::kMC || r.method == cdk::kCATS) {
+                const bool cats = r.method == cdk::kCATS;
+                ck(cdk::launch_indicator_mc_fast(L, S, xc, n, r.tau, yc, mo, io, c, cats), "indicator_mc");
+                mark(0);
+                ck(cdk::launch_sparse_fast(L, S, r.method, false, xc, n, yc, ao, c), "sparse_mc");
+                mark(1);
                 launches += 2;
             } else {
                 ck(cdk::launch_latent_fast(L, S, xc, n, c), "latent");
+                mark(0);
                 ck(cdk::launch_indicator_dc_fast(L, S, n, r.tau, r.ovr ? r.ovr + c0 * F : nullptr, yc, mo, io, c),
                    "indicator_dc");
+                mark(1);
                 ck(cdk::launch_sparse_fast(L, S, cdk::kDC, false, xc, n, yc, ao, c), "sparse_dc");
+                mark(2);
                 launches += 3;
             }
         }
@@ -189,7 +208,7 @@ int run_chain(cd_layer* h, const Req& r) {
         float* ind = r.ind_out ? r.ind_out + c0 * F : S.ind;
         const float* u_full = nullptr;
         if (r.with_masks) {
-            if (r.method == cdk::kMC) u_full = r.u_in + c0 * F;
+            if (r.method == cdk::kMC || r.method == cdk::kCATS) u_full = r.u_in + c0 * F;
             ck(cdk::launch_exact_compact(L, S, 2, nullptr, r.masks_in + c0 * F, n, 0.0f, mo, ao, c), "compact");
             launches += 1;
         } else if (r.method == cdk::kDense) {
@@ -200,6 +219,13 @@ int run_chain(cd_layer* h, const Req& r) {
             ck(cdk::launch_exact_compact(L, S, 0, ind, nullptr, n, r.tau, mo, ao, c), "compact");
             u_full = ind;
             launches += 2;
+        } else if (r.method == cdk::kCATS) {
+            // pipeline_cats (blocked_exec.cpp:330-348): gate pass, act, |act| > tau
+            ck(cdk::launch_exact_rowdot_all(L.w_gate, L.dtype, F, L.rs, d, xc, d, n, ind, F, c), "rowdot_gate");
+            ck(cdk::launch_exact_act(L.act, ind, (int64_t)n * F, c), "act");
+            ck(cdk::launch_exact_compact(L, S, 0, ind, nullptr, n, r.tau, mo, ao, c), "compact");
+            u_full = ind;
+            launches += 3;
         } else {
             ck(cdk::launch_exact_latent(L, S, xc, n, c), "latent_exact");
             ck(cdk::launch_exact_rowdot_all(L.theta_bt, L.dtype, F, L.ldr, L.r, S.ex_lat, L.ldr, n, ind, F, c),
@@ -549,6 +575,44 @@ int cd_pipeline_mc(cd_layer* h, int64_t batch, const float* x, float tau, int re
     });
 }
 
+int cd_exec_cats(cd_layer* h, int64_t batch, const float* x, const float* act_gate, const uint8_t* mask,
+                 int reduction, float* y) {
+    return guarded([&] {
+        check_common(h, batch, x, y);
+        check_reduction(reduction);
+        if (!act_gate || !mask) fail(CD_ERR_DATA, "exec_cats: act_gate and mask are required");
+        Req r;
+        r.method = cdk::kCATS;
+        r.with_masks = true;
+        r.reduction = reduction;
+        HostIO io;
+        io.x = x;
+        io.y = y;
+        io.u_in = act_gate;
+        io.masks_in = mask;
+        host_call(h, r, batch, io);
+    });
+}
+
+int cd_pipeline_cats(cd_layer* h, int64_t batch, const float* x, float tau, int reduction, float* y,
+                     uint8_t* mask_out, int64_t* alive_out, float* act_out) {
+    return guarded([&] {
+        check_common(h, batch, x, y);
+        check_reduction(reduction);
+        Req r;
+        r.method = cdk::kCATS;
+        r.tau = tau;
+        r.reduction = reduction;
+        HostIO io;
+        io.x = x;
+        io.y = y;
+        io.mask_out = mask_out;
+        io.alive_out = alive_out;
+        io.ind_out = act_out;
+        host_call(h, r, batch, io);
+    });
+}
+
 int cd_pipeline_dc(cd_layer* h, int64_t batch, const float* x, float tau_d, const uint8_t* mask_override,
                    int reduction, float* y, uint8_t* mask_out, int64_t* alive_out, float* logits_out) {
     return guarded([&] {
@@ -603,7 +667,8 @@ int cd_forward_device(cd_layer* h, int method, int64_t batch, const float* d_x, 
     return guarded([&] {
         check_common(h, batch, d_x, d_y);
         check_reduction(reduction);
-        if (method != CD_METHOD_DENSE && method != CD_METHOD_MC && method != CD_METHOD_DC)
+        if (method != CD_METHOD_DENSE && method != CD_METHOD_MC && method != CD_METHOD_DC &&
+            method != CD_METHOD_CATS)
             fail(CD_ERR_DATA, "unknown method");
         if (d_mask_override && method != CD_METHOD_DC) fail(CD_ERR_DATA, "mask override is DC-only");
         std::lock_guard<std::mutex> g(h->mu);
@@ -673,6 +738,52 @@ int cd_bench_device(cd_layer* h, int method, int64_t batch, const float* x, floa
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         ck(err, "bench");
+    });
+}
+
+int cd_bench_stages(cd_layer* const* hs, int n_handles, int method, int64_t batch, const float* d_x,
+                    float tau, int64_t warmup, int64_t iters, int64_t* stage_ns_out, int* n_stages_out) {
+    return guarded([&] {
+        if (!hs || n_handles <= 0) fail(CD_ERR_DATA, "bench_stages: no handles");
+        for (int i = 0; i < n_handles; ++i) check_layer(hs[i]);
+        if (batch <= 0 || batch > kMaxBatchFast) fail(CD_ERR_DATA, "bench_stages: batch must be in [1, 4]");
+        if (!d_x || !stage_ns_out || iters <= 0 || warmup < 0) fail(CD_ERR_DATA, "bench_stages: bad arguments");
+        if (method != CD_METHOD_DENSE && method != CD_METHOD_MC && method != CD_METHOD_DC)
+            fail(CD_ERR_DATA, "unknown method");
+        const int nst = method == CD_METHOD_DC ? 3 : method == CD_METHOD_MC ? 2 : 1;
+        cd_layer* h0 = hs[0];
+        ck(cudaSetDevice(h0->device), "cudaSetDevice");
+        cudaStream_t s = h0->stream;
+        cudaEvent_t ev[4];
+        for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+        std::vector<double> acc(nst, 0.0);
+        cudaError_t err = cudaSuccess;
+        for (int64_t it = 0; it < warmup + iters && err == cudaSuccess; ++it) {
+            cd_layer* h = hs[it % n_handles];
+            std::lock_guard<std::mutex> g(h->mu);
+            Req r;
+            r.method = method;
+            r.nb = static_cast<int>(batch);
+            r.x = d_x;
+            r.tau = tau;
+            r.y = h->d_y;
+            r.alive_out = h->d_alive;
+            r.stream = s;
+            r.marks = ev + 1;
+            ck(cudaEventRecord(ev[0], s), "event");
+            run_chain(h, r);
+            err = cudaEventSynchronize(ev[nst]);
+            if (it < warmup) continue;
+            for (int k = 0; k < nst && err == cudaSuccess; ++k) {
+                float ms = 0.0f;
+                err = cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+                acc[k] += static_cast<double>(ms) * 1e6;
+            }
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        ck(err, "bench_stages");
+        for (int k = 0; k < nst; ++k) stage_ns_out[k] = static_cast<int64_t>(acc[k]);
+        if (n_stages_out) *n_stages_out = nst;
     });
 }
 

@@ -60,7 +60,7 @@ struct LaunchCfg {
 };
 
 // Indicator kinds
-enum Method : int { kDense = 0, kMC = 1, kDC = 2 };
+enum Method : int { kDense = 0, kMC = 1, kDC = 2, kCATS = 3 };
 
 // ---------------------------------------------------------------- fast path (UnorderedAccumulate)
 // DC: latent = x theta_a (split over d rows, vector reductions into the zeroed latent).
@@ -72,9 +72,10 @@ cudaError_t launch_indicator_dc_fast(const LayerDev& L, const Scratch& S, int nb
                                      const uint8_t* mask_override, float* y, uint8_t* mask_out,
                                      float* logits_out, const LaunchCfg& c);
 // MC indicator: u = W_up x per neuron, threshold |u| > tau, compaction (u kept per entry).
+// cats=true: CATS indicator h = act(W_gate x), threshold |h| > tau, h kept per entry.
 cudaError_t launch_indicator_mc_fast(const LayerDev& L, const Scratch& S, const float* x, int nb,
                                      float tau, float* y, uint8_t* mask_out, float* u_out,
-                                     const LaunchCfg& c);
+                                     const LaunchCfg& c, bool cats = false);
 // Fused sparse FFN over the compacted list: gathered up/gate rows (DC) or gate rows (MC,
 // u from the list), act inline, row-sparse W_down accumulate; y += via red.v4.
 // dense=true processes every row (count = F) without a list.
@@ -99,10 +100,12 @@ cudaError_t launch_exact_rowdot_all(const void* W, int dtype, int64_t nrows, int
 cudaError_t launch_exact_compact(const LayerDev& L, const Scratch& S, int mode,
                                  const float* ind, const uint8_t* masks_in, int nb, float tau,
                                  uint8_t* mask_out, int* alive_out, const LaunchCfg& c);
-// Phase 1 over the list: DC/dense s = up * act(gate); MC s = act(gate) * u.
+// Phase 1 over the list: DC/dense s = up * act(gate); MC s = act(gate) * u; CATS s = up * h.
 cudaError_t launch_exact_phase1(const LayerDev& L, const Scratch& S, int method,
                                 const float* x, const float* u_full, int nb,
                                 const LaunchCfg& c);
+// v[i] = act(v[i]) in place, double precision / one rounding (numerics.cpp:47-67).
+cudaError_t launch_exact_act(int act, float* v, int64_t n, const LaunchCfg& c);
 // y[b][j] = fold over list (ascending neuron) of s * W_down[i][j] for alive samples.
 cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,
                               const LaunchCfg& c);

@@ -159,6 +159,12 @@ __global__ void ke_phase1(LayerDev L, Scratch S, int method, const float* __rest
             float g = 0.0f;
             for (int64_t j = 0; j < L.d; ++j) g = __fadd_rn(g, __fmul_rn(ldw(wg + j), xb[j]));
             s = __fmul_rn(act_exact(L.act, g), u_full[b * L.F + i]);
+        } else if (method == kCATS) {
+            // exec_cats (blocked_exec.cpp:227-243): s = (W_up[i] . x) * act_gate[i]
+            const W* wu = static_cast<const W*>(L.w_up) + i * L.rs;
+            float u = 0.0f;
+            for (int64_t j = 0; j < L.d; ++j) u = __fadd_rn(u, __fmul_rn(ldw(wu + j), xb[j]));
+            s = __fmul_rn(u, u_full[b * L.F + i]);
         } else {
             const W* wu = static_cast<const W*>(L.w_up) + i * L.rs;
             float u = 0.0f, g = 0.0f;
@@ -170,6 +176,13 @@ __global__ void ke_phase1(LayerDev L, Scratch S, int method, const float* __rest
         }
     }
     S.ex_s[(int64_t)b * L.F + slot] = s;
+}
+
+// ============================================================================ exact activation
+// pipeline_cats (blocked_exec.cpp:338-341): act[i] = apply_activation(gate[i]), in place.
+__global__ void ke_act(int act, float* __restrict__ v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = act_exact(act, v[i]);
 }
 
 // ============================================================================ exact down projection
@@ -269,6 +282,11 @@ cudaError_t launch_exact_phase1(const LayerDev& L, const Scratch& S, int method,
     if (L.dtype == kBF16)
         return launch_ex(ke_phase1<__nv_bfloat16>, grid, dim3(128), 0, c, false, L, S, method, x, u_full);
     return launch_ex(ke_phase1<float>, grid, dim3(128), 0, c, false, L, S, method, x, u_full);
+}
+
+cudaError_t launch_exact_act(int act, float* v, int64_t n, const LaunchCfg& c) {
+    const int blocks = static_cast<int>(imin64(1024, (n + 255) / 256));
+    return launch_ex(ke_act, dim3(blocks), dim3(256), 0, c, false, act, v, n);
 }
 
 cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,

@@ -23,6 +23,7 @@ namespace cdk {
 namespace {
 
 constexpr int kStageBytesTarget = 32 * 1024;
+constexpr int kMC_ = kMC, kDC_ = kDC, kCATS_ = kCATS;  // Method ids usable where kMC is shadowed
 constexpr int kSmemBudget = 200 * 1024;
 
 __device__ __forceinline__ int64_t ldcg_i64(const int64_t* p) { return __ldcg(p); }
@@ -266,7 +267,7 @@ __global__ void k_indicator_dc(LayerDev L, Scratch S, int nb, int rows_per_cta, 
 // in registers; a stage holds kSR consecutive W_up rows (one bulk copy).
 constexpr int kSR = 4;
 
-template <typename W, int NB, int VPT>
+template <typename W, int NB, int VPT, bool kCats>
 __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __restrict__ x,
                                int rows_per_cta, int nstages, float tau, float* __restrict__ y,
                                int64_t y_len, uint8_t* __restrict__ mask_out,
@@ -308,7 +309,9 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
         y[i] = 0.0f;
     __syncthreads();
 
-    const W* U = static_cast<const W*>(L.w_up);
+    // M-CountDown thresholds u = W_up x; CATS (pipeline_cats blocked_exec.cpp:330-348)
+    // thresholds h = act(W_gate x) and keeps h for the up-row phase.
+    const W* U = static_cast<const W*>(kCats ? L.w_gate : L.w_up);
     if (warp == nwc) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
@@ -386,6 +389,7 @@ __global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __res
                     float u = 0.0f;
                     if (valid)
                         for (int w = 0; w < nwc; ++w) u += rb[w * kV + lane * NB + b];
+                    if (kCats) u = act_fast(L.act, u);
                     uv[b] = u;
                     bool a = false;
                     if (valid && b < nb) {
@@ -442,13 +446,22 @@ struct SlotMeta {
     float u[kMaxBatchFast];
 };
 
-template <typename W, int NB, int VPT, bool kMC>
+// KIND: kDC  s = (W_up[i].x) act(W_gate[i].x)           copies [up|gate|down]
+//       kMC  s = act(W_gate[i].x) u_i (u from the list)   copies [gate|down]
+//       kCATS s = (W_up[i].x) h_i (h = act(gate) from the list) copies [up|gate|down] (the gate
+//             row rides along unused: CATS is a comparison baseline, not the hot path)
+template <typename W, int NB, int VPT, int KIND>
 __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict__ x, int nstages,
                          bool dense, float* __restrict__ y, int* __restrict__ alive_out) {
+    constexpr bool kMC = KIND == kMC_;
+    constexpr bool kOneDot = KIND != kDC_;    // one dot product per neuron (MC, CATS)
+    constexpr bool kListU = KIND != kDC_;     // per-sample factor comes from the list
     constexpr int kTl = kMC ? 3 : 2;
     if (threadIdx.x == 0) TL(kTl, 0);
     extern __shared__ __align__(1024) uint8_t smem[];
-    constexpr int kRows = kMC ? 2 : 3;  // rows per neuron: (up,) gate, down
+    constexpr int kRows = kMC ? 2 : 3;  // rows per neuron copied: (up,) gate, down
+    constexpr int kDotRow = KIND == kDC_ ? 1 : 0;   // row of the (first) dot: DC gate, MC gate, CATS up
+    constexpr int kDownRow = kMC ? 1 : 2;
     const int nwc = blockDim.x / kWarp - 1;
     const int nc = nwc * kWarp;
     const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
@@ -503,7 +516,7 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
                 } else {
                     my_i = __ldcg(S.list + my);
                     my_bits = __ldcg(S.bits + my);
-                    if (kMC) {
+                    if (kListU) {
 #pragma unroll
                         for (int b = 0; b < NB; ++b) my_u[b] = __ldcg(S.list_val + (int64_t)my * kMaxBatchFast + b);
                     }
@@ -553,7 +566,7 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
         // warp 0 alone finishes the cross-warp sums and the activation (no redundant work in
         // the other warps), a second barrier publishes s, then every column owner
         // accumulates s * W_down[i] into its register-resident y with FFMA2.
-        constexpr int kM = kMC ? 1 : 2;            // gate (, up) sums per neuron
+        constexpr int kM = kOneDot ? 1 : 2;        // dot products per neuron
         constexpr int kV = kGroup * kM * NB;       // partial sums per lane per group
         int st = 0;
         uint32_t ph = 0;
@@ -573,20 +586,20 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
                     if (threadIdx.x == 0 && it == 0 && q == 0) TL(kTl, 2);
                     const uint8_t* sbase = smem + st * stage_bytes;
                     const W* rup = reinterpret_cast<const W*>(sbase);
-                    const W* rgate = reinterpret_cast<const W*>(sbase + (kMC ? 0 : row_bytes));
+                    const W* rgate = reinterpret_cast<const W*>(sbase + kDotRow * row_bytes);
 #pragma unroll
                     for (int j = 0; j < VPT; ++j) {
                         const int vec = ct + j * nc;
                         if (vec < nvec) {
                             float wg[8], wu[8];
                             Vec8<W>::load(rgate + vec * kVec, wg);
-                            if (!kMC) Vec8<W>::load(rup + vec * kVec, wu);
+                            if (!kOneDot) Vec8<W>::load(rup + vec * kVec, wu);
 #pragma unroll
                             for (int b = 0; b < NB; ++b)
 #pragma unroll
                                 for (int k = 0; k < 8; k += 2) {
                                     ffma2(g0[b], g1[b], wg[k], wg[k + 1], xr[b][j][k], xr[b][j][k + 1]);
-                                    if (!kMC) ffma2(u0[b], u1[b], wu[k], wu[k + 1], xr[b][j][k], xr[b][j][k + 1]);
+                                    if (!kOneDot) ffma2(u0[b], u1[b], wu[k], wu[k + 1], xr[b][j][k], xr[b][j][k + 1]);
                                 }
                         }
                     }
@@ -595,7 +608,7 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
 #pragma unroll
                 for (int b = 0; b < NB; ++b) {
                     v[(q * kM) * NB + b] = g0[b] + g1[b];
-                    if (!kMC) v[(q * kM + 1) * NB + b] = u0[b] + u1[b];
+                    if (!kOneDot) v[(q * kM + 1) * NB + b] = u0[b] + u1[b];
                 }
             }
             const float tot = warp_transpose_sum<kV>(v);
@@ -606,14 +619,18 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
                 float g = 0.0f, u = 0.0f;
                 for (int w = 0; w < nwc; ++w) {
                     g += red[w * kV + (q * kM) * NB + b];
-                    if (!kMC) u += red[w * kV + (q * kM + 1) * NB + b];
+                    if (!kOneDot) u += red[w * kV + (q * kM + 1) * NB + b];
                 }
                 int sq = sts[0];
 #pragma unroll
                 for (int qq = 1; qq < kGroup; ++qq) sq = (q == qq) ? sts[qq] : sq;
-                if (kMC) u = meta[sq].u[b];
+                if (kListU) u = meta[sq].u[b];
                 const bool alive = (meta[sq].bits >> b) & 1u;
-                sval[lane] = alive ? (kMC ? act_fast(L.act, g) * u : u * act_fast(L.act, g)) : 0.0f;
+                float sv = 0.0f;
+                if (KIND == kDC_) sv = u * act_fast(L.act, g);
+                else if (KIND == kMC_) sv = act_fast(L.act, g) * u;
+                else sv = g * u;  // CATS: up dot times the list's act(gate)
+                sval[lane] = alive ? sv : 0.0f;
             }
             named_bar_sync(1, nc);
 #pragma unroll
@@ -623,7 +640,7 @@ __global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict_
                     float sv[NB];
 #pragma unroll
                     for (int b = 0; b < NB; ++b) sv[b] = sval[q * NB + b];
-                    const W* rdown = reinterpret_cast<const W*>(smem + sq * stage_bytes + (kMC ? 1 : 2) * row_bytes);
+                    const W* rdown = reinterpret_cast<const W*>(smem + sq * stage_bytes + kDownRow * row_bytes);
 #pragma unroll
                     for (int j = 0; j < VPT; ++j) {
                         const int vec = ct + j * nc;
@@ -784,7 +801,7 @@ cudaError_t launch_indicator_dc_fast(const LayerDev& L, const Scratch& S, int nb
 #undef CD_DC_CASES
 }
 
-template <typename W, int NB>
+template <typename W, int NB, bool kCats>
 static cudaError_t dispatch_mc_vpt(int nb, int vpt, const LayerDev& L, const Scratch& S, const float* x,
                                    int rpc, int nstages, float tau, float* y, int64_t y_len,
                                    uint8_t* mask_out, float* u_out, size_t smem, int threads,
@@ -796,17 +813,26 @@ static cudaError_t dispatch_mc_vpt(int nb, int vpt, const LayerDev& L, const Scr
                          y_len, mask_out, u_out);
     };
     switch (vpt) {
-        case 1: return go(k_indicator_mc<W, NB, 1>);
-        case 2: return go(k_indicator_mc<W, NB, 2>);
-        case 4: if constexpr (NB <= 2) return go(k_indicator_mc<W, NB, 4>); else return cudaErrorInvalidValue;
-        case 8: if constexpr (NB == 1) return go(k_indicator_mc<W, NB, 8>); else return cudaErrorInvalidValue;
+        case 1: return go(k_indicator_mc<W, NB, 1, kCats>);
+        case 2: return go(k_indicator_mc<W, NB, 2, kCats>);
+        case 4: if constexpr (NB <= 2) return go(k_indicator_mc<W, NB, 4, kCats>); else return cudaErrorInvalidValue;
+        case 8: if constexpr (NB == 1) return go(k_indicator_mc<W, NB, 8, kCats>); else return cudaErrorInvalidValue;
     }
     return cudaErrorInvalidValue;
 }
 
+template <typename W, bool kCats>
+static cudaError_t dispatch_mc(int nb, int nbk, int vpt, const LayerDev& L, const Scratch& S, const float* x,
+                               int rpc, int nstages, float tau, float* y, int64_t y_len, uint8_t* mask_out,
+                               float* u_out, size_t smem, int threads, const LaunchCfg& c) {
+    if (nbk == 1) return dispatch_mc_vpt<W, 1, kCats>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
+    if (nbk == 2) return dispatch_mc_vpt<W, 2, kCats>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
+    return dispatch_mc_vpt<W, 4, kCats>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
+}
+
 cudaError_t launch_indicator_mc_fast(const LayerDev& L, const Scratch& S, const float* x, int nb,
                                      float tau, float* y, uint8_t* mask_out, float* u_out,
-                                     const LaunchCfg& c) {
+                                     const LaunchCfg& c, bool cats) {
     const int64_t nvec = L.ld / kVec;
     const int vpt = choose_vpt(nvec);
     if (vpt < 0) return cudaErrorInvalidValue;
@@ -824,16 +850,14 @@ cudaError_t launch_indicator_mc_fast(const LayerDev& L, const Scratch& S, const 
                         (size_t)rpc * (8 + 4 * nbk) + 64;
     const int64_t y_len = (int64_t)nb * L.d;
     if (L.dtype == kBF16) {
-        if (nbk == 1) return dispatch_mc_vpt<__nv_bfloat16, 1>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
-        if (nbk == 2) return dispatch_mc_vpt<__nv_bfloat16, 2>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
-        return dispatch_mc_vpt<__nv_bfloat16, 4>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
+        if (cats) return dispatch_mc<__nv_bfloat16, true>(nb, nbk, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
+        return dispatch_mc<__nv_bfloat16, false>(nb, nbk, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
     }
-    if (nbk == 1) return dispatch_mc_vpt<float, 1>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
-    if (nbk == 2) return dispatch_mc_vpt<float, 2>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
-    return dispatch_mc_vpt<float, 4>(nb, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
+    if (cats) return dispatch_mc<float, true>(nb, nbk, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
+    return dispatch_mc<float, false>(nb, nbk, vpt, L, S, x, rpc, nstages, tau, y, y_len, mask_out, u_out, smem, threads, c);
 }
 
-template <typename W, int NB, bool kMC>
+template <typename W, int NB, int KIND>
 static cudaError_t dispatch_sparse_vpt(int nb, int vpt, const LayerDev& L, const Scratch& S, const float* x,
                                        int nstages, bool dense, float* y, int* alive_out, size_t smem,
                                        int threads, const LaunchCfg& c) {
@@ -844,26 +868,32 @@ static cudaError_t dispatch_sparse_vpt(int nb, int vpt, const LayerDev& L, const
                          alive_out);
     };
     switch (vpt) {
-        case 1: return go(k_sparse<W, NB, 1, kMC>);
-        case 2: return go(k_sparse<W, NB, 2, kMC>);
-        case 4: if constexpr (NB <= 2) return go(k_sparse<W, NB, 4, kMC>); else return cudaErrorInvalidValue;
-        case 8: if constexpr (NB == 1) return go(k_sparse<W, NB, 8, kMC>); else return cudaErrorInvalidValue;
+        case 1: return go(k_sparse<W, NB, 1, KIND>);
+        case 2: return go(k_sparse<W, NB, 2, KIND>);
+        case 4: if constexpr (NB <= 2) return go(k_sparse<W, NB, 4, KIND>); else return cudaErrorInvalidValue;
+        case 8: if constexpr (NB == 1) return go(k_sparse<W, NB, 8, KIND>); else return cudaErrorInvalidValue;
     }
     return cudaErrorInvalidValue;
 }
 
+template <typename W, int KIND>
+static cudaError_t dispatch_sparse_kind(int nb, int nbk, int vpt, const LayerDev& L, const Scratch& S,
+                                        const float* x, int nstages, bool dense, float* y, int* alive_out,
+                                        size_t smem, int threads, const LaunchCfg& c) {
+    if (nbk == 1) return dispatch_sparse_vpt<W, 1, KIND>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
+    if (nbk == 2) return dispatch_sparse_vpt<W, 2, KIND>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
+    return dispatch_sparse_vpt<W, 4, KIND>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
+}
+
 template <typename W>
-static cudaError_t dispatch_sparse(int nb, int nbk, bool mc, int vpt, const LayerDev& L, const Scratch& S,
+static cudaError_t dispatch_sparse(int nb, int nbk, int method, int vpt, const LayerDev& L, const Scratch& S,
                                    const float* x, int nstages, bool dense, float* y, int* alive_out,
                                    size_t smem, int threads, const LaunchCfg& c) {
-    if (mc) {
-        if (nbk == 1) return dispatch_sparse_vpt<W, 1, true>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
-        if (nbk == 2) return dispatch_sparse_vpt<W, 2, true>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
-        return dispatch_sparse_vpt<W, 4, true>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
-    }
-    if (nbk == 1) return dispatch_sparse_vpt<W, 1, false>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
-    if (nbk == 2) return dispatch_sparse_vpt<W, 2, false>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
-    return dispatch_sparse_vpt<W, 4, false>(nb, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
+    if (method == kMC)
+        return dispatch_sparse_kind<W, kMC>(nb, nbk, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
+    if (method == kCATS)
+        return dispatch_sparse_kind<W, kCATS>(nb, nbk, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
+    return dispatch_sparse_kind<W, kDC>(nb, nbk, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
 }
 
 cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, bool dense,
@@ -890,8 +920,8 @@ cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, 
         if (e != cudaSuccess) return e;
     }
     if (L.dtype == kBF16)
-        return dispatch_sparse<__nv_bfloat16>(nb, nbk, mc, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
-    return dispatch_sparse<float>(nb, nbk, mc, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
+        return dispatch_sparse<__nv_bfloat16>(nb, nbk, method, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
+    return dispatch_sparse<float>(nb, nbk, method, vpt, L, S, x, nstages, dense, y, alive_out, smem, threads, c);
 }
 
 }  // namespace cdk

@@ -357,3 +357,45 @@ def test_device_forward_graph_capture(oracle):
     _, z = oracle.lowrank_logits(g["theta_a"], g["theta_b"], g["x"])
     want = oracle.forward_sparse(g, g["x"], (z > 0).astype(np.uint8))
     assert rel_l2(y.cpu().numpy(), want) <= 1e-4
+
+
+# ----------------------------------------------------------------------------- reference's own tests
+def test_reference_unit_tests_on_gpu_shim():
+    """The reference's doctest suites (test_blocked_exec / test_sparsity / test_numerics /
+    test_gated_mlp / test_costmodel / test_predictor / test_calibration) linked against
+    paper_2505_17701_b200/shim/blocked_exec_gpu.cpp -- every exec_* / pipeline_* / bench call
+    runs on the B200 through the C-ABI -- must all pass."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_unit_tests_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ref_unit_tests_gpu not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "0 failed" in r.stdout
+
+
+# ----------------------------------------------------------------------------- CATS baseline
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("act", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES[:5])
+def test_cats_pipeline(oracle, shape, act, dtype):
+    """pipeline_cats / exec_cats (blocked_exec.cpp:214-250, 330-348): s = (W_up x) act(gate),
+    mask |act(gate)| > tau -- bitwise forward_sparse in the exact mode."""
+    seed, d, F, r = shape
+    g, layer, _ = make_case(oracle, seed, d, F, r, act, dtype)
+    x = g["x"]
+    tr = oracle.forward_dense(g, x, act=act)
+    tau = top_m_tau(tr["h"], max(1, F // 3))
+    want_mask = (np.abs(tr["h"]) > tau).astype(np.uint8)
+    want = oracle.forward_sparse(g, x, want_mask, act=act)
+    got = cd.pipeline_cats(layer, x, tau, ORD, want_act=True)
+    assert bits_equal(got.act, tr["h"])
+    assert np.array_equal(got.mask.alive, want_mask)
+    assert bits_equal(got.y, want)
+    assert bits_equal(cd.exec_cats(layer, x, tr["h"], want_mask, ORD), want)
+    fast = cd.pipeline_cats(layer, x, tau, FAST, want_act=True)
+    check_mask_flips(fast.mask.alive, want_mask, tr["h"], tau, 1e-4)
+    assert rel_l2(fast.y, oracle.forward_sparse(g, x, fast.mask.alive, act=act)) <= 1e-4
+    assert rel_l2(cd.exec_cats(layer, x, tr["h"], want_mask, FAST), want) <= 1e-4

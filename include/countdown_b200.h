@@ -184,8 +184,9 @@ CD_API int cd_bench_device(cd_layer* h, int method, int64_t batch, const float* 
  * `warmup + iters` times, rotating over the n_handles layers (so a layer's rows are evicted
  * from L2 between its uses when the handles together exceed L2), with programmatic dependent
  * launch OFF and a CUDA event after every kernel.  stage_ns_out[k] receives the SUM over the
- * timed iterations of stage k's time; *n_stages_out the number of stages (DC 3: latent,
- * indicator, sparse FFN; MC 2: indicator, sparse FFN; dense 1).  d_x: batch x d_model device
+ * timed iterations of stage k's time; *n_stages_out the number of stages (DC: 1, the fused
+ * persistent kernel, or 3 -- latent, indicator, sparse FFN -- where the fused kernel does not
+ * cover the shape; MC 2: indicator, sparse FFN; dense 1).  d_x: batch x d_model device
  * f32.  Used for the roofline of the dominant kernel; the bench's headline rate is timed
  * with the chain PDL-overlapped (cd_forward_device in a CUDA graph). */
 CD_API int cd_bench_stages(cd_layer* const* hs, int n_handles, int method, int64_t batch,

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -62,6 +63,8 @@ struct cd_layer {
     std::vector<void*> host_allocs;
     int64_t bytes = 0;
     int last_launches = 0;
+    bool use_fused = true;  // D-CountDown as one persistent kernel (CD_DC_CHAIN=1 forces the chain)
+    int keep0 = 3;          // fused kernel: own active neurons streamed before rebalancing (CD_KEEP0)
     // device staging for the host-buffer entry points
     float* d_x = nullptr;
     float* d_y = nullptr;
@@ -184,7 +187,13 @@ int run_chain(cd_layer* h, const Req& r) {
                 ck(cdk::launch_sparse_fast(L, S, r.method, false, xc, n, yc, ao, c), "sparse_mc");
                 mark(1);
                 launches += 2;
+            } else if (h->use_fused &&
+                       cdk::launch_dc_fused(L, S, xc, n, r.tau, r.ovr ? r.ovr + c0 * F : nullptr, yc, mo, io, ao,
+                                            c, h->keep0) == cudaSuccess) {
+                launches += 1;
+                mark(0);
             } else {
+                (void)cudaGetLastError();  // an unsupported fused shape: use the chain
                 ck(cdk::launch_latent_fast(L, S, xc, n, c), "latent");
                 mark(0);
                 ck(cdk::launch_indicator_dc_fast(L, S, n, r.tau, r.ovr ? r.ovr + c0 * F : nullptr, yc, mo, io, c),
@@ -388,6 +397,12 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     S.count = h->dalloc<int>(1);
     S.done = h->dalloc<int>(1);
     S.alive = h->dalloc<int>(kMaxBatch);
+    S.ctl = h->dalloc<unsigned>(128);
+    S.t_list = h->dalloc<unsigned long long>(L.F);
+    S.t_count = h->dalloc<unsigned long long>(cdk::kMaxCtas);
+    S.t_alive = h->dalloc<unsigned long long>(cdk::kMaxCtas * kMaxBatchFast);
+    if (const char* env = std::getenv("CD_DC_CHAIN")) h->use_fused = env[0] != '1';
+    if (const char* env = std::getenv("CD_KEEP0")) h->keep0 = std::atoi(env);
     S.ind = h->dalloc<float>(kMaxBatch * L.F);
     S.ex_s = h->dalloc<float>(kMaxBatch * L.F);
     h->d_x = h->dalloc<float>(kMaxBatch * d);
@@ -453,26 +468,39 @@ int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, co
         if (ldr / cdk::kVecElems > 256) fail(CD_ERR_DATA, "predictor: d_rank > 2048 is not supported");
         const size_t esz = L.dtype == CD_DTYPE_BF16 ? 2 : 4;
         void* ta = h->dalloc<uint8_t>(static_cast<size_t>(L.d * ldr) * esz, false);
+        void* tat = h->dalloc<uint8_t>(static_cast<size_t>(d_rank * L.ld) * esz, false);
         void* tbt = h->dalloc<uint8_t>(static_cast<size_t>(L.F * ldr) * esz, false);
         float* tmp = nullptr;
         const size_t tmp_n = static_cast<size_t>(std::max(L.d * d_rank, d_rank * h->F_total));
         ck(cudaMalloc(&tmp, sizeof(float) * tmp_n), "cudaMalloc tmp");
         cudaError_t e = cudaMemcpyAsync(tmp, theta_a, sizeof(float) * L.d * d_rank, cudaMemcpyHostToDevice, h->stream);
         if (e == cudaSuccess) e = cdk::launch_pack_rows(tmp, L.d, d_rank, d_rank, ta, L.dtype, ldr, ldr, h->stream);
+        if (e == cudaSuccess)
+            e = cdk::launch_pack_transpose(tmp, L.d, d_rank, 0, d_rank, tat, L.dtype, L.ld, h->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(tmp, theta_b, sizeof(float) * d_rank * h->F_total, cudaMemcpyHostToDevice, h->stream);
         if (e == cudaSuccess)
             e = cdk::launch_pack_transpose(tmp, d_rank, h->F_total, h->row_begin, L.F, tbt, L.dtype, ldr, h->stream);
+        void* tfrag = nullptr;
+        const int64_t kst = (d_rank + 15) / 16;
+        if (e == cudaSuccess && L.dtype == CD_DTYPE_BF16) {
+            tfrag = h->dalloc<uint8_t>(static_cast<size_t>((L.F + 15) / 16 * kst * 512), false);
+            e = cdk::launch_pack_frag_bt(tmp, d_rank, h->F_total, h->row_begin, L.F, tfrag, h->stream);
+        }
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         cudaFree(tmp);
         ck(e, "predictor upload");
         if (!h->S.latent) h->S.latent = h->dalloc<float>(kMaxBatch * 2048);
         if (!h->S.ex_lat) h->S.ex_lat = h->dalloc<float>(kMaxBatch * 2048);
+        if (!h->S.t_lat) h->S.t_lat = h->dalloc<unsigned long long>(kMaxBatchFast * 2048);
         L.r = d_rank;
         L.ldr = ldr;
         L.theta_a = ta;
+        L.theta_at = tat;
         L.theta_bt = tbt;
+        L.theta_bt_frag = tfrag;
+        L.kst = kst;
     });
 }
 
@@ -750,7 +778,7 @@ int cd_bench_stages(cd_layer* const* hs, int n_handles, int method, int64_t batc
         if (!d_x || !stage_ns_out || iters <= 0 || warmup < 0) fail(CD_ERR_DATA, "bench_stages: bad arguments");
         if (method != CD_METHOD_DENSE && method != CD_METHOD_MC && method != CD_METHOD_DC)
             fail(CD_ERR_DATA, "unknown method");
-        const int nst = method == CD_METHOD_DC ? 3 : method == CD_METHOD_MC ? 2 : 1;
+        int nst = method == CD_METHOD_DC ? 3 : method == CD_METHOD_MC ? 2 : 1;
         cd_layer* h0 = hs[0];
         ck(cudaSetDevice(h0->device), "cudaSetDevice");
         cudaStream_t s = h0->stream;
@@ -770,8 +798,10 @@ int cd_bench_stages(cd_layer* const* hs, int n_handles, int method, int64_t batc
             r.alive_out = h->d_alive;
             r.stream = s;
             r.marks = ev + 1;
+            ck(cdk::launch_spin(30000ull, s), "spin");  // host enqueues the timed work meanwhile
             ck(cudaEventRecord(ev[0], s), "event");
-            run_chain(h, r);
+            const int nl = run_chain(h, r);
+            if (method == CD_METHOD_DC) nst = nl;  // 1 when the fused kernel ran, 3 for the chain
             err = cudaEventSynchronize(ev[nst]);
             if (it < warmup) continue;
             for (int k = 0; k < nst && err == cudaSuccess; ++k) {
@@ -792,6 +822,9 @@ CD_API int cd_debug_timeline(unsigned long long* out, int64_t n) {
     return guarded([&] {
         ck(cudaDeviceSynchronize(), "sync");
         ck(cdk::read_timeline(out, n), "timeline");
+        std::vector<unsigned long long> f(static_cast<size_t>(n));
+        ck(cdk::read_timeline_fused(f.data(), n), "timeline");
+        for (int64_t i = 0; i < n; ++i) out[i] += f[static_cast<size_t>(i)];
     });
 }
 #endif

@@ -110,6 +110,25 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float b0, float b1, 
         : "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
 
+// Warp-level bf16 tensor-core MMA, D(16x8, f32) += A(16x16, row) * B(16x8, col).  Fragment
+// layout (lane = 4g + t): a0 = A[g][2t..2t+1], a1 = A[g+8][2t..], a2 = A[g][2t+8..],
+// a3 = A[g+8][2t+8..]; b0 = B[2t..2t+1][g], b1 = B[2t+8..2t+9][g]; d0,d1 = D[g][2t..2t+1],
+// d2,d3 = D[g+8][2t..2t+1].  Used for the predictor GEMV of the fused decode kernel, where it
+// removes the bf16 unpack + FMA instruction stream (the stage is latency-, not FLOP-bound).
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint4& a, const uint2& b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+        "{%8, %9}, {%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y));
+}
+
+// Two floats -> bf16x2 (RNE), the first in the low half.
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
 // ---------------------------------------------------------------- global reductions
 // red.global.add.v4.f32 (sm_90+): one vector reduction instead of four scalar atomics.
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {

@@ -25,6 +25,7 @@ namespace cdk {
 constexpr int kVecElems = 8;      // weights per 16-byte (bf16) vector unit; row stride multiple
 constexpr int kMaxBatchFast = 4;   // samples per fused-kernel instance (union of masks)
 constexpr int kMaxBatch = 32;      // samples per call (bitmask width)
+constexpr int kMaxCtas = 1024;     // fused kernel grid bound (== SM count)
 
 struct LayerDev {
     int64_t d = 0, F = 0, ld = 0;  // d_model, rows in this shard, padded row length
@@ -35,7 +36,13 @@ struct LayerDev {
     const void* w_down = nullptr;
     int64_t r = 0, ldr = 0;
     const void* theta_a = nullptr;   // d x ldr
+    const void* theta_at = nullptr;  // r x ld  (theta_a transposed: one latent column per row)
     const void* theta_bt = nullptr;  // F x ldr
+    // bf16 layers: theta_bt re-arranged in mma.sync m16n8k16 A-fragment order, tile by tile:
+    // tile T (rows 16T..16T+15) x k-step s (columns 16s..16s+15) is 512 contiguous bytes,
+    // lane l's 16 bytes = its {a0, a1, a2, a3} (zero-padded past F and r).  kst = ceil(r/16).
+    const void* theta_bt_frag = nullptr;
+    int64_t kst = 0;
 };
 
 // Per-handle device scratch.  latent/count/done are "self-cleaning": every kernel
@@ -51,6 +58,12 @@ struct Scratch {
     float* ind = nullptr;          // kMaxBatch x F : exact-mode indicator (u or logits)
     float* ex_s = nullptr;         // kMaxBatch x F : exact-mode s
     float* ex_lat = nullptr;       // kMaxBatch x ldr : exact-mode latent
+    // fused kernel (kernels_fused.cu): epoch-tagged words {payload, launch tag}
+    unsigned* ctl = nullptr;                  // [0] launch tag of the last completed launch
+    unsigned long long* t_lat = nullptr;      // kMaxBatchFast x 2048 : latent values
+    unsigned long long* t_list = nullptr;     // F : rest-list entries (neuron id | bits << 27)
+    unsigned long long* t_count = nullptr;    // kMaxCtas : rest-list length per CTA
+    unsigned long long* t_alive = nullptr;    // kMaxCtas x kMaxBatchFast : alive counts per CTA
 };
 
 struct LaunchCfg {
@@ -82,6 +95,14 @@ cudaError_t launch_indicator_mc_fast(const LayerDev& L, const Scratch& S, const 
 cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, bool dense,
                                const float* x, int nb, float* y, int* alive_out,
                                const LaunchCfg& c);
+// D-CountDown step as one persistent kernel (kernels_fused.cu): latent, predictor, threshold,
+// compaction and the sparse FFN with grid barriers; zeroes and accumulates y, writes
+// alive_out.  keep0: active neurons of its own chunk each CTA streams before the global
+// rebalancing.  Returns cudaErrorInvalidValue for shapes it does not cover (the caller then
+// uses the three-kernel chain).
+cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
+                            const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
+                            int* alive_out, const LaunchCfg& c, int keep0 = 3);
 // Host-supplied masks (exec_mc / exec_dc): ordered compaction + zero y (+ MC u gather).
 cudaError_t launch_compact_masks(const LayerDev& L, const Scratch& S, const uint8_t* masks,
                                  const float* u_full, int nb, float* y, const LaunchCfg& c);
@@ -110,13 +131,20 @@ cudaError_t launch_exact_act(int act, float* v, int64_t n, const LaunchCfg& c);
 cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,
                               const LaunchCfg& c);
 
+// One-thread kernel that occupies the stream for `ns` nanoseconds (timing helper).
+cudaError_t launch_spin(unsigned long long ns, cudaStream_t s);
+
 // Development build only (-DCD_TIMELINE): copy the per-CTA phase stamps to the host.
 cudaError_t read_timeline(unsigned long long* out, int64_t n);
+cudaError_t read_timeline_fused(unsigned long long* out, int64_t n);
 
 // ---------------------------------------------------------------- layout helpers
 // dst row r = src row r (cols values, zero-padded to ld_pad), rows ld_dst apart.
 cudaError_t launch_pack_rows(const float* src, int64_t rows, int64_t cols, int64_t ld_src,
                              void* dst, int dtype, int64_t ld_pad, int64_t ld_dst, cudaStream_t s);
+// theta_bt_frag (see LayerDev) from the f32 theta_b (r x ld_src), columns [col_begin, +F).
+cudaError_t launch_pack_frag_bt(const float* theta_b, int64_t r, int64_t ld_src, int64_t col_begin,
+                                int64_t F, void* dst, cudaStream_t s);
 // dst (cols_sel x ldr) = transpose of src[:, col_begin:col_begin+cols_sel] (src rows x ld_src).
 cudaError_t launch_pack_transpose(const float* src, int64_t rows, int64_t ld_src,
                                   int64_t col_begin, int64_t cols_sel, void* dst, int dtype,

@@ -36,6 +36,17 @@ __global__ void k_zero(float* __restrict__ p, int64_t n) {
         p[i] = 0.0f;
 }
 
+// ============================================================================ spin
+// Keeps the stream busy for `ns` nanoseconds (stage timing: the host enqueues the timed work
+// while this runs, so CUDA events measure device time, not host launch latency).
+__global__ void k_spin(unsigned long long ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
 // ============================================================================ latent
 // latent[b][q] += sum_{i in this CTA's rows} x[b][i] * theta_a[i][q]; reduced in smem then one
 // vector reduction per column group per CTA.  theta_a rows are read once, coalesced.
@@ -734,6 +745,11 @@ cudaError_t read_timeline(unsigned long long*, int64_t) { return cudaErrorNotSup
 #endif
 
 // ---------------------------------------------------------------- public launchers
+cudaError_t launch_spin(unsigned long long ns, cudaStream_t s) {
+    k_spin<<<1, 32, 0, s>>>(ns);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_latent_fast(const LayerDev& L, const Scratch& S, const float* x, int nb,
                                const LaunchCfg& c) {
     if (L.ldr / kVec > 256) return cudaErrorInvalidValue;

@@ -1,0 +1,806 @@
+// kernels_fused.cu -- the D-CountDown decode step as ONE persistent sm_100a kernel.
+//
+// pipeline_dc (blocked_exec.cpp:350-379) / Alg. 3 with UnorderedAccumulate
+// semantics.  One CTA per SM.  Every weight byte is streamed by the TMA bulk-copy engine into
+// shared memory; the step's three dependent stages exchange data between CTAs through
+// EPOCH-TAGGED 64-bit words ({payload, launch tag} written with one single-copy-atomic store,
+// readers spin until the tag matches) instead of grid barriers: there is no fence on the
+// critical path, so no CTA ever waits for its own in-flight bulk copies to drain (a release
+// fence does: measured 1.5-4.5 us per grid barrier with TMA traffic in flight).
+//
+//   prologue  (before griddepcontrol.wait -- overlaps the previous grid's tail)
+//             producer lane streams this CTA's theta_at slice (its latent columns) and its
+//             theta_bt chunk (its neurons' predictor rows, one contiguous run).
+//   stage 1   latent[q] = theta_at[q] . x for q in this CTA's columns (predictor.cpp:94-102);
+//             each value is published as a tagged word.
+//   stage 2   all CTAs gather the latent (spinning on the tags), s_hat_i = latent . theta_bt[i]
+//             for the chunk's neurons (predictor.cpp:104-113), threshold s_hat > tau_D or the
+//             mask override, CTA-local ballot compaction.  The first K0 active neurons are KEPT
+//             and start streaming at once; the rest are published as tagged list words plus a
+//             tagged per-CTA count.
+//   stage 3   every CTA reads the G counts, and takes ranks c, c+G, c+2G, ... of the concatenated
+//             rest lists (balanced to one record).  A neuron's record [up | gate | down] is ONE
+//             contiguous bulk copy; s_i = up act(gate) (exec_dc blocked_exec.cpp:263-281) and
+//             y += s_i W_down[i] accumulate in registers of the column-owning consumer threads;
+//             one red.global.add.v4 per owned column group at the end.
+//
+// y is zeroed by CTA G-1 (no latent work at the Llama shape) and published by a fence before its
+// count word, which every CTA acquires before its reductions.  The launch tag is read at start
+// (after griddepcontrol.wait) and advanced by CTA 0 at its end: CTA 0 cannot finish before every
+// CTA has published its count, i.e. read the tag.
+//
+// Requirements: grid == number of SMs, one CTA per SM (the dynamic shared memory forces it), all
+// CTAs co-resident (the spins wait on other CTAs).
+#include <type_traits>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "launch.cuh"
+
+namespace cdk {
+
+namespace {
+
+constexpr int kRBf = 8;       // predictor rows per warp iteration (stage 2)
+constexpr int kGroupF = 4;    // neurons per reduction round (stage 3)
+constexpr int kSmemBudgetF = 220 * 1024;
+constexpr int kCtlEpoch = 0;  // ctl word: launch tag of the last completed launch
+
+struct MetaF {
+    int32_t idx;
+    uint32_t bits;
+};
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long tagged(uint32_t tag, uint32_t payload) {
+    return (static_cast<unsigned long long>(tag) << 32) | payload;
+}
+
+// Spin until the word carries `tag`; return its payload.
+__device__ __forceinline__ uint32_t await_relaxed(const unsigned long long* p, uint32_t tag) {
+    unsigned long long w;
+    do {
+        w = ld_relaxed_u64(p);
+    } while (static_cast<uint32_t>(w >> 32) != tag);
+    return static_cast<uint32_t>(w);
+}
+
+__device__ __forceinline__ uint32_t await_acquire(const unsigned long long* p, uint32_t tag) {
+    unsigned long long w;
+    do {
+        w = ld_acquire_u64(p);
+    } while (static_cast<uint32_t>(w >> 32) != tag);
+    return static_cast<uint32_t>(w);
+}
+
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Kernel arguments in one block (read through the constant bank as instruction operands).
+struct FusedParams {
+    LayerDev L;
+    Scratch S;
+    const float* x;
+    const uint8_t* ovr;
+    float* y;
+    uint8_t* mask_out;
+    float* logits_out;
+    int* alive_out;
+    float tau;
+    int nb, nstages, rows_per_cta, keep0, qrows;
+};
+
+template <typename W, int NB, int VPT, int VPL>
+__global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ FusedParams P) {
+    // bf16 layers run the predictor GEMV on the tensor cores (theta_bt in A-fragment order)
+    constexpr bool kMma = std::is_same<W, __nv_bfloat16>::value;
+    const LayerDev& L = P.L;
+    const Scratch& S = P.S;
+    const int nb = P.nb, nstages = P.nstages, rows_per_cta = P.rows_per_cta, qrows = P.qrows;
+    const float tau = P.tau;
+    const float* __restrict__ x = P.x;
+    const uint8_t* __restrict__ ovr = P.ovr;
+    float* __restrict__ y = P.y;
+    uint8_t* __restrict__ mask_out = P.mask_out;
+    float* __restrict__ logits_out = P.logits_out;
+    if (threadIdx.x == 0) TL(5, 0);
+#ifdef CD_TIMELINE
+    const long long clk0 = clock64();
+#endif
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int kBarC = 1;   // consumers only
+    constexpr int kBarK = 3;   // consumers -> producer: own list, counts and launch tag in smem
+    constexpr int kBarT = 5;   // producer -> consumers: rest-list prefix in smem
+    const int nwc = blockDim.x / kWarp - 1;
+    const int nc = nwc * kWarp;
+    const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    const int G = gridDim.x;
+    const int64_t rec_bytes = 3 * L.ld * (int64_t)sizeof(W);   // one neuron record
+    const int64_t stage_bytes = rec_bytes;
+    // one predictor row in the chunk: ldr elements (f32 row layout) or kst*16 (fragment layout)
+    const int64_t brow_bytes = kMma ? L.kst * 32 : L.ldr * (int64_t)sizeof(W);
+    const int64_t arow_bytes = L.ld * (int64_t)sizeof(W);      // one theta_at row
+
+    // ---- shared memory carve-up (all offsets multiples of 16).  The theta_at slice and x live
+    // at the END of the ring (the predictor rows occupy its start): both are dead before the
+    // first neuron record is streamed, so the whole ring serves stage 3.
+    uint8_t* ring = smem;
+    const int64_t aux_bytes = arow_bytes * qrows;
+    W* abuf = reinterpret_cast<W*>(ring + stage_bytes * nstages - aux_bytes);  // [qrows][ld]
+    float* latbuf = reinterpret_cast<float*>(ring + stage_bytes * nstages);    // [NB][ldr]
+    uint64_t* full = reinterpret_cast<uint64_t*>(latbuf + NB * L.ldr);
+    uint64_t* empty = full + nstages;
+    uint64_t* bar_a = empty + nstages;
+    uint64_t* bar_b = bar_a + 2;
+    MetaF* meta = reinterpret_cast<MetaF*>(bar_a + 3);
+    int32_t* own_idx = reinterpret_cast<int32_t*>(meta + nstages);
+    uint32_t* own_bits = reinterpret_cast<uint32_t*>(own_idx + rows_per_cta);
+    float* red = reinterpret_cast<float*>(own_bits + rows_per_cta);  // [nwc][32] warp partials
+    float* sval = red + nwc * 32;                                      // [kGroupF * NB]
+    int* cnt = reinterpret_cast<int*>(sval + kGroupF * NB);           // [0] n_own [1..NB] alive [NB+1] tag
+    int* pre = cnt + 2 + NB;                                           // [G + 1] prefix of rest counts
+    uint2* latfrag = reinterpret_cast<uint2*>(
+        (reinterpret_cast<uintptr_t>(pre + G + 1) + 15) & ~static_cast<uintptr_t>(15));  // [kst][32] B fragments
+
+    const int64_t c0 = (int64_t)blockIdx.x * rows_per_cta;
+    const int64_t c1 = imin64(L.F, c0 + rows_per_cta);
+    const int nrows = c1 > c0 ? static_cast<int>(c1 - c0) : 0;
+    const int q0 = blockIdx.x * qrows;                      // this CTA's latent columns [q0, q1)
+    const int q1 = min(static_cast<int>(L.r), q0 + qrows);
+    const int nq = q1 > q0 ? q1 - q0 : 0;
+    // the kept records are issued into a fresh ring: never more than it holds
+    const int keep0 = min(P.keep0, nstages);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nstages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], nwc);
+        }
+        mbar_init(bar_a, 1);
+        mbar_init(bar_b, 1);
+        for (int b = 0; b <= NB; ++b) cnt[b] = 0;
+        fence_mbar_init();
+    }
+    __syncthreads();
+    pdl_launch_dependents();
+
+    const uint8_t* BT = static_cast<const uint8_t*>(kMma ? L.theta_bt_frag : L.theta_bt);
+    const W* AT = static_cast<const W*>(L.theta_at);
+    const W* REC = static_cast<const W*>(L.w_up);   // records [up | gate | down], stride L.rs
+
+    if (warp == nwc) {
+        // ================================================================ producer warp
+        const uint64_t pol = policy_evict_first();
+        int st = 0;
+        uint32_t ph = 0;
+        if (lane == 0) {
+            // prologue: weights only (step-independent), overlaps the previous grid's tail
+            if (nq > 0) {
+                mbar_arrive_expect_tx(bar_a, static_cast<uint32_t>(nq * arow_bytes));
+                bulk_g2s(abuf, AT + (int64_t)q0 * L.ld, static_cast<uint32_t>(nq * arow_bytes), bar_a, pol);
+            }
+            if (nrows > 0) {
+                // rows_per_cta is a multiple of 16 in the fragment layout: whole tiles
+                const int64_t bytes = kMma ? (nrows + 15) / 16 * 16 * brow_bytes : nrows * brow_bytes;
+                mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bytes));
+                bulk_g2s(ring, BT + c0 * brow_bytes, static_cast<uint32_t>(bytes), bar_b, pol);
+            }
+        }
+        __syncwarp();
+        auto issue = [&](int32_t i, uint32_t bits) {
+            mbar_wait(&empty[st], ph ^ 1);
+            meta[st].idx = i;
+            meta[st].bits = bits;
+            mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rec_bytes));
+            bulk_g2s(ring + st * stage_bytes, REC + (int64_t)i * L.rs, static_cast<uint32_t>(rec_bytes), &full[st],
+                     pol);
+            if (++st == nstages) { st = 0; ph ^= 1; }
+        };
+        // kept neurons of this CTA's own chunk: stream them while the other CTAs finish stage 2
+        named_bar_sync(kBarK, nc + kWarp);
+        const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
+        const int kept = min(cnt[0], keep0);
+        if (lane == 0) TL(6, 5);
+        if (lane == 0)
+            for (int e = 0; e < kept; ++e) issue(own_idx[e], own_bits[e]);
+        if (lane == 0) TL(6, 6);
+        __syncwarp();
+        // rest-list counts of every CTA: all of a lane's words are requested at once (relaxed
+        // loads -- an acquire load would hold back every later load), only stale ones re-polled
+        int run = 0;
+        for (int i0 = 0; i0 < G; i0 += 8 * kWarp) {
+            unsigned long long w[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + k * kWarp + lane;
+                w[k] = i < G ? ld_relaxed_u64(S.t_count + i) : tagged(tag, 0u);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + k * kWarp + lane;
+                if (static_cast<uint32_t>(w[k] >> 32) != tag) w[k] = tagged(tag, await_relaxed(S.t_count + i, tag));
+                int v = static_cast<int>(static_cast<uint32_t>(w[k]));
+#pragma unroll
+                for (int o = 1; o < kWarp; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o) v += u;
+                }
+                if (i < G) pre[i + 1] = run + v;
+                run += __shfl_sync(0xffffffffu, v, kWarp - 1);
+            }
+        }
+        // acquire CTA G-1's count (seen above): its fence published the zeroed y
+        if (lane == 0) (void)await_acquire(S.t_count + (G - 1), tag);
+        __syncwarp();
+        if (lane == 0) pre[0] = 0;
+        __syncwarp();
+        if (lane == 0) TL(6, 4);
+        named_bar_arrive(kBarT, nc + kWarp);  // consumers may size stage 3 now
+        const int total = run;
+        // balanced share: ranks c, c+G, c+2G, ... of the concatenated rest lists
+        for (int base = blockIdx.x; base < total; base += kWarp * G) {
+            const int my = base + lane * G;
+            int32_t my_i = 0;
+            uint32_t my_b = 0;
+            if (my < total) {
+                int lo = 0, hi = G;  // owner o: pre[o] <= my < pre[o + 1]
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (pre[mid] <= my) lo = mid; else hi = mid;
+                }
+                const uint32_t wv = await_relaxed(S.t_list + (int64_t)lo * rows_per_cta + (my - pre[lo]), tag);
+                my_i = static_cast<int32_t>(wv & ((1u << 27) - 1u));
+                my_b = wv >> 27;
+            }
+            const int n = min(kWarp, (total - base + G - 1) / G);
+            for (int k = 0; k < n; ++k) {
+                const int32_t i = __shfl_sync(0xffffffffu, my_i, k);
+                const uint32_t bits = __shfl_sync(0xffffffffu, my_b, k);
+                if (lane == 0) issue(i, bits);
+                __syncwarp();
+            }
+        }
+    } else {
+        // ================================================================ consumer warps
+        const int ct = threadIdx.x;
+        const int nvec = static_cast<int>(L.ld / kVec);
+        pdl_wait();  // y and the scratch words of the previous step are now safe to touch
+        if (threadIdx.x == 0) {
+            TL(5, 1);
+            cnt[NB + 1] = static_cast<int>(static_cast<uint32_t>(__ldcg(S.ctl + kCtlEpoch)) + 1u);
+        }
+        if (blockIdx.x == G - 1) {
+            for (int64_t i = ct; i < (int64_t)nb * L.d; i += nc) y[i] = 0.0f;
+            named_bar_sync(kBarC, nc);
+            if (threadIdx.x == 0) __threadfence();  // ordered before this CTA's count word
+        }
+        named_bar_sync(kBarC, nc);
+        const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
+        // x into registers (column ownership: vectors ct + j*nc).  Plain vector loads, not the
+        // TMA engine: a bulk copy of x would queue behind this CTA's predictor prefetch.
+        float xr[NB][VPT][8];
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int vec = ct + j * nc;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+                const int64_t col = (int64_t)vec * kVec;
+                if (vec < nvec && b < nb) {
+                    const float4* src = reinterpret_cast<const float4*>(x + b * L.d + col);
+                    if (col < L.d) lo = __ldcg(src);
+                    if (col + 4 < L.d) hi = __ldcg(src + 1);
+                }
+                xr[b][j][0] = lo.x; xr[b][j][1] = lo.y; xr[b][j][2] = lo.z; xr[b][j][3] = lo.w;
+                xr[b][j][4] = hi.x; xr[b][j][5] = hi.y; xr[b][j][6] = hi.z; xr[b][j][7] = hi.w;
+            }
+        }
+        if (threadIdx.x == 0) TL(6, 2);
+
+        // ---------------------------------------------------------- stage 1: latent columns
+        if (nq > 0) {
+            mbar_wait(bar_a, 0);
+            if (threadIdx.x == 0) TL(6, 3);
+            constexpr int kQ = 4;
+            for (int qb = 0; qb < nq; qb += kQ) {
+                float v[kQ * NB];
+#pragma unroll
+                for (int qq = 0; qq < kQ; ++qq) {
+                    float a0[NB], a1[NB];
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0f;
+                    if (qb + qq < nq) {
+#pragma unroll
+                        for (int j = 0; j < VPT; ++j) {
+                            const int vec = ct + j * nc;
+                            if (vec < nvec) {
+                                float w[8];
+                                Vec8<W>::load(abuf + (int64_t)(qb + qq) * L.ld + vec * kVec, w);
+#pragma unroll
+                                for (int b = 0; b < NB; ++b)
+#pragma unroll
+                                    for (int k = 0; k < 8; k += 2) ffma2(a0[b], a1[b], w[k], w[k + 1], xr[b][j][k], xr[b][j][k + 1]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) v[qq * NB + b] = a0[b] + a1[b];
+                }
+                constexpr int kV = kQ * NB;
+                const float tot = warp_transpose_sum<kV>(v);
+                if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
+                named_bar_sync(kBarC, nc);
+                if (warp == 0 && lane < kV) {
+                    const int qq = lane / NB, b = lane % NB;
+                    float s = 0.0f;
+                    for (int w = 0; w < nwc; ++w) s += red[w * 32 + lane];
+                    if (qb + qq < nq && b < nb)
+                        st_relaxed_u64(S.t_lat + b * L.ldr + q0 + qb + qq, tagged(tag, __float_as_uint(s)));
+                }
+                named_bar_sync(kBarC, nc);
+            }
+        }
+        if (threadIdx.x == 0) TL(5, 2);
+
+        // ---------------------------------------------------------- stage 2: predictor + compaction
+        // gather the latent (every CTA published its columns as tagged words): all of a thread's
+        // words are requested at once, stale ones re-polled
+        for (int e0 = ct; e0 < NB * (int)L.ldr; e0 += 4 * nc) {
+            unsigned long long w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int e = e0 + k * nc;
+                const int b = e / (int)L.ldr, q = e % (int)L.ldr;
+                w[k] = (e < NB * (int)L.ldr && b < nb && q < L.r) ? ld_relaxed_u64(S.t_lat + e) : tagged(tag, 0u);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int e = e0 + k * nc;
+                if (e >= NB * (int)L.ldr) continue;
+                if (static_cast<uint32_t>(w[k] >> 32) != tag) w[k] = tagged(tag, await_relaxed(S.t_lat + e, tag));
+                latbuf[e] = __uint_as_float(static_cast<uint32_t>(w[k]));
+            }
+        }
+        named_bar_sync(kBarC, nc);
+        if (threadIdx.x == 0) TL(5, 3);
+#ifdef CD_TIMELINE
+        long long clk_s2 = 0;
+#endif
+        if constexpr (kMma) {
+            // B fragments of the latent: column g of the 16x8 B tile is sample g/2, split into a
+            // bf16 high part (g even) and the bf16 of the remainder (g odd): ~16-bit precision
+            for (int e = ct; e < L.kst * 32; e += nc) {
+                const int s = e >> 5, l = e & 31, g = l >> 2, t = l & 3;
+                uint2 v = make_uint2(0u, 0u);
+                if (g < 2 * NB) {
+                    const int b = g >> 1;
+                    const int k = 16 * s + 2 * t;
+                    float f[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int kk = k + (u & 1) + (u >> 1) * 8;
+                        const float val = kk < L.r ? latbuf[b * L.ldr + kk] : 0.0f;
+                        const float hiv = __bfloat162float(__float2bfloat16_rn(val));
+                        f[u] = (g & 1) ? val - hiv : hiv;
+                    }
+                    v.x = pack_bf16x2(f[0], f[1]);
+                    v.y = pack_bf16x2(f[2], f[3]);
+                }
+                latfrag[e] = v;
+            }
+            named_bar_sync(kBarC, nc);
+            if (nrows > 0) mbar_wait(bar_b, 0);
+            if (threadIdx.x == 0) TL(6, 0);
+#ifdef CD_TIMELINE
+            clk_s2 = clock64();
+#endif
+            const int g = lane >> 2, t = lane & 3;
+            const int ntile = (nrows + 15) / 16;
+            for (int tt = warp; tt < ntile; tt += nwc) {
+                float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
+                const uint4* A = reinterpret_cast<const uint4*>(ring + (int64_t)tt * L.kst * 512) + lane;
+                const uint2* B = latfrag + lane;
+                int s = 0;
+#pragma unroll 4
+                for (; s + 1 < L.kst; s += 2) {
+                    mma_bf16_16816(acc0, A[s * 32], B[s * 32]);
+                    mma_bf16_16816(acc1, A[(s + 1) * 32], B[(s + 1) * 32]);
+                }
+                if (s < L.kst) mma_bf16_16816(acc0, A[s * 32], B[s * 32]);
+                // lane (g, t): rows g and g+8 of the tile, sample t (its hi + lo columns)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float z = h ? (acc0[2] + acc0[3]) + (acc1[2] + acc1[3])
+                                      : (acc0[0] + acc0[1]) + (acc1[0] + acc1[1]);
+                    const int rl = tt * 16 + g + 8 * h;
+                    const bool valid = rl < nrows;
+                    const int64_t gi = c0 + rl;
+                    bool a = false;
+                    if (valid && t < nb) {
+                        a = ovr ? (ovr[t * L.F + gi] != 0) : (z > tau);
+                        if (mask_out) mask_out[t * L.F + gi] = a ? 1 : 0;
+                        if (logits_out) logits_out[t * L.F + gi] = z;
+                    }
+                    uint32_t bits = static_cast<uint32_t>(a) << t;
+                    bits |= __shfl_xor_sync(0xffffffffu, bits, 1);
+                    bits |= __shfl_xor_sync(0xffffffffu, bits, 2);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        const unsigned bal = __ballot_sync(0xffffffffu, a && t == b);
+                        if (lane == 0 && bal) atomicAdd(&cnt[1 + b], __popc(bal));
+                    }
+                    const bool take = t == 0 && bits != 0;
+                    const unsigned any = __ballot_sync(0xffffffffu, take);
+                    int e0 = 0;
+                    if (lane == 0 && any) e0 = atomicAdd(&cnt[0], __popc(any));
+                    e0 = __shfl_sync(0xffffffffu, e0, 0);
+                    if (take) {
+                        const int e = e0 + __popc(any & ((1u << lane) - 1u));
+                        own_idx[e] = static_cast<int32_t>(gi);
+                        own_bits[e] = bits;
+                    }
+                }
+            }
+        } else {
+        float lat[NB][VPL][8];
+        const int nvr = static_cast<int>(L.ldr / kVec);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+            const int vec = lane + v * kWarp;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+                if (vec < nvr) {
+                    const float4* src = reinterpret_cast<const float4*>(latbuf + b * L.ldr + vec * kVec);
+                    lo = src[0];
+                    hi = src[1];
+                }
+                lat[b][v][0] = lo.x; lat[b][v][1] = lo.y; lat[b][v][2] = lo.z; lat[b][v][3] = lo.w;
+                lat[b][v][4] = hi.x; lat[b][v][5] = hi.y; lat[b][v][6] = hi.z; lat[b][v][7] = hi.w;
+            }
+        }
+        if (nrows > 0) mbar_wait(bar_b, 0);
+        if (threadIdx.x == 0) TL(6, 0);
+        {
+            const W* base = reinterpret_cast<const W*>(ring);
+            for (int rr0 = warp * kRBf; rr0 < nrows; rr0 += nwc * kRBf) {
+                constexpr int kV = kRBf * NB;
+                float v[kV];
+#pragma unroll
+                for (int j = 0; j < kRBf; ++j) {
+                    float w[VPL][8];
+#pragma unroll
+                    for (int q = 0; q < VPL; ++q) {
+                        const int vec = lane + q * kWarp;
+                        if (rr0 + j < nrows && vec < nvr) Vec8<W>::load(base + (rr0 + j) * L.ldr + vec * kVec, w[q]);
+                        else
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) w[q][k] = 0.0f;
+                    }
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+                        for (int q = 0; q < VPL; ++q)
+#pragma unroll
+                            for (int k = 0; k < 8; k += 2) ffma2(a0, a1, w[q][k], w[q][k + 1], lat[b][q][k], lat[b][q][k + 1]);
+                        v[j * NB + b] = a0 + a1;
+                    }
+                }
+                const float tot = warp_transpose_sum<kV>(v);
+                if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
+                __syncwarp();
+                const bool valid = lane < kRBf && rr0 + lane < nrows;
+                const int64_t gi = c0 + rr0 + lane;
+                uint32_t bits = 0;
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    bool a = false;
+                    if (valid && b < nb) {
+                        const float z = red[warp * 32 + lane * NB + b];
+                        a = ovr ? (ovr[b * L.F + gi] != 0) : (z > tau);
+                        if (mask_out) mask_out[b * L.F + gi] = a ? 1 : 0;
+                        if (logits_out) logits_out[b * L.F + gi] = z;
+                    }
+                    bits |= static_cast<uint32_t>(a) << b;
+                    const unsigned bal = __ballot_sync(0xffffffffu, a);
+                    if (lane == 0 && bal) atomicAdd(&cnt[1 + b], __popc(bal));
+                }
+                const unsigned any = __ballot_sync(0xffffffffu, bits != 0);
+                int e0 = 0;
+                if (lane == 0 && any) e0 = atomicAdd(&cnt[0], __popc(any));
+                e0 = __shfl_sync(0xffffffffu, e0, 0);
+                if (bits) {
+                    const int e = e0 + __popc(any & ((1u << lane) - 1u));
+                    own_idx[e] = static_cast<int32_t>(gi);
+                    own_bits[e] = bits;
+                }
+                __syncwarp();
+            }
+        }
+        }
+        if (threadIdx.x == 0) {
+            TL(6, 1);
+#ifdef CD_TIMELINE
+            if constexpr (kMma)
+                if (blockIdx.x < kTlCtas) g_timeline[7][blockIdx.x][6] = static_cast<unsigned long long>(clock64() - clk_s2);
+#endif
+        }
+        named_bar_sync(kBarC, nc);
+        if (threadIdx.x == 0) TL(5, 4);
+        const int n_own = cnt[0];
+        const int kept = min(n_own, keep0);
+        named_bar_arrive(kBarK, nc + kWarp);  // producer may stream the kept neurons now
+        // publish the rest list, its length and the per-sample alive counts (tagged words)
+        for (int e = kept + ct; e < n_own; e += nc)
+            st_relaxed_u64(S.t_list + c0 + e - kept,
+                           tagged(tag, static_cast<uint32_t>(own_idx[e]) | (own_bits[e] << 27)));
+        if (threadIdx.x == 0) {
+            for (int b = 0; b < NB; ++b)
+                st_relaxed_u64(S.t_alive + blockIdx.x * kMaxBatchFast + b, tagged(tag, static_cast<uint32_t>(cnt[1 + b])));
+            st_relaxed_u64(S.t_count + blockIdx.x, tagged(tag, static_cast<uint32_t>(n_own - kept)));
+        }
+        named_bar_sync(kBarT, nc + kWarp);
+        if (threadIdx.x == 0) TL(5, 5);
+        const int total = pre[G];
+        const int n_rec = kept + (total > (int)blockIdx.x ? (total - (int)blockIdx.x + G - 1) / G : 0);
+        int st = 0;
+        uint32_t ph = 0;
+
+        // ---------------------------------------------------------- stage 3: sparse FFN
+        float yr[NB][VPT][8];
+#pragma unroll
+        for (int j = 0; j < VPT; ++j)
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) yr[b][j][k] = 0.0f;
+        const int64_t row_bytes = L.ld * (int64_t)sizeof(W);
+        for (int g0 = 0; g0 < n_rec; g0 += kGroupF) {
+            const int ns = min(kGroupF, n_rec - g0);
+            constexpr int kV = kGroupF * 2 * NB;
+            int sts[kGroupF];
+            float v[kV];
+#pragma unroll
+            for (int q = 0; q < kGroupF; ++q) {
+                sts[q] = st;
+                float g0v[NB], g1v[NB], u0[NB], u1[NB];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) g0v[b] = g1v[b] = u0[b] = u1[b] = 0.0f;
+                if (q < ns) {
+                    mbar_wait(&full[st], ph);
+                    const uint8_t* sb = ring + st * stage_bytes;
+                    const W* rup = reinterpret_cast<const W*>(sb);
+                    const W* rgate = reinterpret_cast<const W*>(sb + row_bytes);
+#pragma unroll
+                    for (int j = 0; j < VPT; ++j) {
+                        const int vec = ct + j * nc;
+                        if (vec < nvec) {
+                            float wg[8], wu[8];
+                            Vec8<W>::load(rgate + vec * kVec, wg);
+                            Vec8<W>::load(rup + vec * kVec, wu);
+#pragma unroll
+                            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                                for (int k = 0; k < 8; k += 2) {
+                                    ffma2(g0v[b], g1v[b], wg[k], wg[k + 1], xr[b][j][k], xr[b][j][k + 1]);
+                                    ffma2(u0[b], u1[b], wu[k], wu[k + 1], xr[b][j][k], xr[b][j][k + 1]);
+                                }
+                        }
+                    }
+                    if (++st == nstages) { st = 0; ph ^= 1; }
+                }
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    v[(q * 2) * NB + b] = g0v[b] + g1v[b];
+                    v[(q * 2 + 1) * NB + b] = u0[b] + u1[b];
+                }
+            }
+            const float tot = warp_transpose_sum<kV>(v);
+            if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
+            named_bar_sync(kBarC, nc);
+            if (warp == 0 && lane < ns * NB) {
+                const int q = lane / NB, b = lane % NB;
+                float g = 0.0f, u = 0.0f;
+                for (int w = 0; w < nwc; ++w) {
+                    g += red[w * 32 + (q * 2) * NB + b];
+                    u += red[w * 32 + (q * 2 + 1) * NB + b];
+                }
+                int sq = sts[0];
+#pragma unroll
+                for (int qq = 1; qq < kGroupF; ++qq) sq = (q == qq) ? sts[qq] : sq;
+                const bool alive = (meta[sq].bits >> b) & 1u;
+                sval[lane] = alive ? u * act_fast(L.act, g) : 0.0f;
+            }
+            named_bar_sync(kBarC, nc);
+#pragma unroll
+            for (int q = 0; q < kGroupF; ++q) {
+                if (q < ns) {
+                    const int sq = sts[q];
+                    float sv[NB];
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) sv[b] = sval[q * NB + b];
+                    const W* rdown = reinterpret_cast<const W*>(ring + sq * stage_bytes + 2 * row_bytes);
+#pragma unroll
+                    for (int j = 0; j < VPT; ++j) {
+                        const int vec = ct + j * nc;
+                        if (vec < nvec) {
+                            float wd[8];
+                            Vec8<W>::load(rdown + vec * kVec, wd);
+#pragma unroll
+                            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                                for (int k = 0; k < 8; k += 2)
+                                    ffma2(yr[b][j][k], yr[b][j][k + 1], sv[b], sv[b], wd[k], wd[k + 1]);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[sq]);
+                }
+            }
+        }
+        if (threadIdx.x == 0) TL(5, 6);
+        if (n_rec > 0) {
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                const int vec = ct + j * nc;
+                if (vec < nvec) {
+#pragma unroll
+                    for (int b = 0; b < NB; ++b)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (b >= nb) continue;
+                            const int64_t col = (int64_t)vec * kVec + h * 4;
+                            float* dst = y + b * L.d + col;
+                            if (col + 4 <= L.d && ((L.d & 3) == 0)) {
+                                red_add_v4(dst, yr[b][j][h * 4], yr[b][j][h * 4 + 1], yr[b][j][h * 4 + 2],
+                                           yr[b][j][h * 4 + 3]);
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    if (col + k < L.d) red_add_f32(dst + k, yr[b][j][h * 4 + k]);
+                            }
+                        }
+                }
+            }
+        }
+        if (blockIdx.x == 0 && warp == 0) {
+            // per-sample alive counts (sum of the CTAs' tagged counts), then advance the tag:
+            // every CTA read it before publishing the count CTA 0's producer waited for
+            if (P.alive_out)
+                for (int b = 0; b < nb; ++b) {
+                    int a = 0;
+                    for (int i = lane; i < G; i += kWarp)
+                        a += static_cast<int>(await_relaxed(S.t_alive + i * kMaxBatchFast + b, tag));
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                    if (lane == 0) P.alive_out[b] = a;
+                }
+            if (lane == 0) S.ctl[kCtlEpoch] = tag;
+        }
+    }
+    if (threadIdx.x == 0) {
+        TL(5, 7);
+#ifdef CD_TIMELINE
+        if (blockIdx.x < kTlCtas) g_timeline[7][blockIdx.x][7] = static_cast<unsigned long long>(clock64() - clk0);
+#endif
+    }
+}
+
+}  // namespace
+
+#ifdef CD_TIMELINE
+cudaError_t read_timeline_fused(unsigned long long* out, int64_t n) {
+    const size_t cnt = (size_t)kTlKernels * kTlCtas * kTlPhases;
+    if ((size_t)n < cnt) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_timeline, cnt * sizeof(unsigned long long));
+    static unsigned long long zeros[kTlKernels * kTlCtas * kTlPhases];
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_timeline, zeros, sizeof(zeros));
+    return e;
+}
+#else
+cudaError_t read_timeline_fused(unsigned long long*, int64_t) { return cudaErrorNotSupported; }
+#endif
+
+cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
+                            const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
+                            int* alive_out, const LaunchCfg& c, int keep0) {
+    if (!L.theta_at || !S.t_lat || !S.t_list || !S.t_count || !S.t_alive || !S.ctl) return cudaErrorInvalidValue;
+    if (c.num_sms > kMaxCtas || L.F >= (1 << 27)) return cudaErrorInvalidValue;
+    // x rows are staged by the TMA engine: 16-byte aligned rows of a multiple of 16 bytes
+    if (L.d % 4 != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) return cudaErrorInvalidValue;
+    const int64_t nvec = L.ld / kVec;
+    int vpt = 0;
+    for (int v : {1, 2, 4})
+        if ((nvec + v - 1) / v <= 256) { vpt = v; break; }
+    if (vpt == 0) return cudaErrorInvalidValue;
+    const int nvr = static_cast<int>(L.ldr / kVec);
+    const int vpl = nvr <= 32 ? 1 : nvr <= 64 ? 2 : nvr <= 128 ? 4 : 0;
+    if (vpl == 0) return cudaErrorInvalidValue;
+    const int nbk = nb <= 1 ? 1 : (nb <= 2 ? 2 : 4);
+    if (nbk * kRBf > 32 || nbk * kGroupF * 2 > 32 || nbk * vpt > 8) return cudaErrorInvalidValue;
+    const int G = c.num_sms;
+    const bool mma = L.dtype == kBF16;
+    if (mma && (!L.theta_bt_frag || L.kst <= 0)) return cudaErrorInvalidValue;
+    // neuron chunk per CTA: whole 16-row tiles in the fragment layout
+    const int rpc = mma ? static_cast<int>(16 * (((L.F + 15) / 16 + G - 1) / G)) : static_cast<int>((L.F + G - 1) / G);
+    const int qrows = static_cast<int>((L.r + G - 1) / G);
+    const int64_t esz = L.dtype == kBF16 ? 2 : 4;
+    const int64_t stage_bytes = 3 * L.ld * esz;
+    const int64_t brow_bytes = mma ? L.kst * 32 : L.ldr * esz;
+    const int threads = 288;
+    const int nwc = threads / kWarp - 1;
+    // fixed carve-up beside the ring: latent, barriers, meta, lists, scratch, latent fragments
+    // (the theta_at slice is overlaid on the ring's tail)
+    const int64_t aux_bytes = (int64_t)qrows * L.ld * esz;
+    const int64_t fixed = (int64_t)nbk * L.ldr * 4 + 3 * 8 + (int64_t)rpc * 8 + (nwc * 32 + kGroupF * nbk) * 4 +
+                          (2 + nbk) * 4 + (int64_t)(G + 1) * 4 + 16 + (mma ? L.kst * 256 : 0) + 64;
+    const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
+    const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
+    if (nstages < 2) return cudaErrorInvalidValue;
+    if ((int64_t)rpc * brow_bytes + aux_bytes > stage_bytes * nstages) return cudaErrorInvalidValue;
+    const size_t smem = static_cast<size_t>(fixed + per_stage * nstages);
+    auto go = [&](auto kern) {
+        cudaError_t e = set_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        FusedParams p;
+        p.L = L;
+        p.S = S;
+        p.x = x;
+        p.ovr = mask_override;
+        p.y = y;
+        p.mask_out = mask_out;
+        p.logits_out = logits_out;
+        p.alive_out = alive_out;
+        p.tau = tau;
+        p.nb = nb;
+        p.nstages = nstages;
+        p.rows_per_cta = rpc;
+        p.keep0 = keep0;
+        p.qrows = qrows;
+        return launch_ex(kern, dim3(G), dim3(threads), smem, c, true, p);
+    };
+#define CD_FUSED_CASES(W)                                          \
+    switch (nbk * 100 + vpt * 10 + vpl) {                          \
+        case 121: return go(k_dc_fused<W, 1, 2, 1>);               \
+        case 122: return go(k_dc_fused<W, 1, 2, 2>);               \
+        case 124: return go(k_dc_fused<W, 1, 2, 4>);               \
+        case 111: return go(k_dc_fused<W, 1, 1, 1>);               \
+        case 112: return go(k_dc_fused<W, 1, 1, 2>);               \
+        case 114: return go(k_dc_fused<W, 1, 1, 4>);               \
+        case 141: return go(k_dc_fused<W, 1, 4, 1>);               \
+        case 142: return go(k_dc_fused<W, 1, 4, 2>);               \
+        case 221: return go(k_dc_fused<W, 2, 2, 1>);               \
+        case 222: return go(k_dc_fused<W, 2, 2, 2>);               \
+        case 211: return go(k_dc_fused<W, 2, 1, 1>);               \
+        case 212: return go(k_dc_fused<W, 2, 1, 2>);               \
+        case 241: return go(k_dc_fused<W, 2, 4, 1>);               \
+        case 242: return go(k_dc_fused<W, 2, 4, 2>);               \
+        case 421: return go(k_dc_fused<W, 4, 2, 1>);               \
+        case 422: return go(k_dc_fused<W, 4, 2, 2>);               \
+        case 411: return go(k_dc_fused<W, 4, 1, 1>);               \
+        case 412: return go(k_dc_fused<W, 4, 1, 2>);               \
+    }                                                              \
+    return cudaErrorInvalidValue;
+    if (L.dtype == kBF16) { CD_FUSED_CASES(__nv_bfloat16) }
+    CD_FUSED_CASES(float)
+#undef CD_FUSED_CASES
+}
+
+}  // namespace cdk

@@ -13,7 +13,7 @@ import paper_2505_17701_b200 as cd  # noqa: E402
 from paper_2505_17701_b200 import _capi  # noqa: E402
 
 K, CT, P = 8, 160, 8
-NAMES = {0: "latent", 1: "ind_dc", 2: "sparse_dc", 3: "sparse_mc", 4: "ind_mc"}
+NAMES = {0: "latent", 1: "ind_dc", 2: "sparse_dc", 3: "sparse_mc", 4: "ind_mc", 5: "dc_fused", 6: "fused_st2", 7: "fused_prod"}
 
 
 def read():
@@ -25,6 +25,17 @@ def read():
 
 
 def show(tl, label):
+    cyc = tl[7, :148, 7].copy()
+    s2 = tl[7, :148, 6].copy()
+    tl[7, :, 7] = 0
+    tl[7, :, 6] = 0
+    if (s2 > 0).any():
+        print(f"    stage-2 loop cycles (thread 0): median {np.median(s2[s2 > 0]):.0f}, max {s2.max():.0f}")
+    if (cyc > 0).any():
+        dur = (tl[5, :148, 7] - tl[5, :148, 0]) / 1e3
+        ok = (cyc > 0) & (dur > 0)
+        print(f"    fused kernel SM clock: median {np.median(cyc[ok] / dur[ok]) / 1e3:.0f} MHz "
+              f"(cycles / globaltimer us over each CTA's lifetime)")
     nz = tl[tl > 0]
     t0 = nz.min()
     print(f"--- {label} (us relative to first stamp)")

@@ -64,7 +64,7 @@ struct cd_layer {
     int64_t bytes = 0;
     int last_launches = 0;
     bool use_fused = true;  // D-CountDown as one persistent kernel (CD_DC_CHAIN=1 forces the chain)
-    int keep0 = 3;          // fused kernel: own active neurons streamed before rebalancing (CD_KEEP0)
+    int keep0 = 0;          // fused kernel: own active neurons streamed before rebalancing (CD_KEEP0)
     // device staging for the host-buffer entry points
     float* d_x = nullptr;
     float* d_y = nullptr;

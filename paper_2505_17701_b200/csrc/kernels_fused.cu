@@ -44,7 +44,10 @@ namespace {
 constexpr int kRBf = 8;       // predictor rows per warp iteration (stage 2)
 constexpr int kGroupF = 4;    // neurons per reduction round (stage 3)
 constexpr int kSmemBudgetF = 220 * 1024;
-constexpr int kCtlEpoch = 0;  // ctl word: launch tag of the last completed launch
+constexpr int kMaxConsumers = 512;  // consumer threads per CTA (16 warps) + one producer warp
+constexpr int kCtlEpoch = 0;    // ctl word: launch tag of the last completed launch
+constexpr int kCtlQueue = 32;   // ctl words: 3 x 32 (launch tag % 3) work-queue counters
+constexpr int kYZeroWord = 1023;  // t_count word: "y zeroed" flag of the launch
 
 struct MetaF {
     int32_t idx;
@@ -61,6 +64,16 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_add_u32(unsigned* p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
@@ -107,7 +120,7 @@ struct FusedParams {
 };
 
 template <typename W, int NB, int VPT, int VPL>
-__global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ FusedParams P) {
     // bf16 layers run the predictor GEMV on the tensor cores (theta_bt in A-fragment order)
     constexpr bool kMma = std::is_same<W, __nv_bfloat16>::value;
     const LayerDev& L = P.L;
@@ -126,7 +139,6 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int kBarC = 1;   // consumers only
     constexpr int kBarK = 3;   // consumers -> producer: own list, counts and launch tag in smem
-    constexpr int kBarT = 5;   // producer -> consumers: rest-list prefix in smem
     const int nwc = blockDim.x / kWarp - 1;
     const int nc = nwc * kWarp;
     const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
@@ -153,10 +165,9 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
     uint32_t* own_bits = reinterpret_cast<uint32_t*>(own_idx + rows_per_cta);
     float* red = reinterpret_cast<float*>(own_bits + rows_per_cta);  // [nwc][32] warp partials
     float* sval = red + nwc * 32;                                      // [kGroupF * NB]
-    int* cnt = reinterpret_cast<int*>(sval + kGroupF * NB);           // [0] n_own [1..NB] alive [NB+1] tag
-    int* pre = cnt + 2 + NB;                                           // [G + 1] prefix of rest counts
+    int* cnt = reinterpret_cast<int*>(sval + kGroupF * NB);  // [0] n_own [1..NB] alive [NB+1] tag [NB+2] cap
     uint2* latfrag = reinterpret_cast<uint2*>(
-        (reinterpret_cast<uintptr_t>(pre + G + 1) + 15) & ~static_cast<uintptr_t>(15));  // [kst][32] B fragments
+        (reinterpret_cast<uintptr_t>(cnt + NB + 3) + 15) & ~static_cast<uintptr_t>(15));  // [kst][32] B fragments
 
     const int64_t c0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t c1 = imin64(L.F, c0 + rows_per_cta);
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
     const int q1 = min(static_cast<int>(L.r), q0 + qrows);
     const int nq = q1 > q0 ? q1 - q0 : 0;
     // the kept records are issued into a fresh ring: never more than it holds
-    const int keep0 = min(P.keep0, nstages);
+    // (P.keep0 is unused: the own-work cap comes from the previous launch)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < nstages; ++s) {
@@ -212,70 +223,62 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
                      pol);
             if (++st == nstages) { st = 0; ph ^= 1; }
         };
-        // kept neurons of this CTA's own chunk: stream them while the other CTAs finish stage 2
+        // ---- stage 3 schedule: this CTA's own active neurons up to the cap, its overflow
+        // published to the launch's work queue, then stealing from that queue until empty.
         named_bar_sync(kBarK, nc + kWarp);
         const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
-        const int kept = min(cnt[0], keep0);
-        if (lane == 0) TL(6, 5);
-        if (lane == 0)
-            for (int e = 0; e < kept; ++e) issue(own_idx[e], own_bits[e]);
-        if (lane == 0) TL(6, 6);
-        __syncwarp();
-        // rest-list counts of every CTA: all of a lane's words are requested at once (relaxed
-        // loads -- an acquire load would hold back every later load), only stale ones re-polled
-        int run = 0;
-        for (int i0 = 0; i0 < G; i0 += 8 * kWarp) {
-            unsigned long long w[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int i = i0 + k * kWarp + lane;
-                w[k] = i < G ? ld_relaxed_u64(S.t_count + i) : tagged(tag, 0u);
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int i = i0 + k * kWarp + lane;
-                if (static_cast<uint32_t>(w[k] >> 32) != tag) w[k] = tagged(tag, await_relaxed(S.t_count + i, tag));
-                int v = static_cast<int>(static_cast<uint32_t>(w[k]));
-#pragma unroll
-                for (int o = 1; o < kWarp; o <<= 1) {
-                    const int u = __shfl_up_sync(0xffffffffu, v, o);
-                    if (lane >= o) v += u;
-                }
-                if (i < G) pre[i + 1] = run + v;
-                run += __shfl_sync(0xffffffffu, v, kWarp - 1);
-            }
+        const int n_own = cnt[0];
+        const int kept = min(n_own, cnt[NB + 2]);
+        const int ovf = n_own - kept;
+        unsigned* qc = S.ctl + kCtlQueue + (tag % 3u) * 32u;  // [0] tail [1] head [2] pushed [3] actives
+        int e = 0;
+        if (lane == 0) {
+            TL(6, 5);
+            for (; e < min(kept, nstages); ++e) issue(own_idx[e], own_bits[e]);  // fresh ring: no wait
         }
-        // acquire CTA G-1's count (seen above): its fence published the zeroed y
-        if (lane == 0) (void)await_acquire(S.t_count + (G - 1), tag);
-        __syncwarp();
-        if (lane == 0) pre[0] = 0;
-        __syncwarp();
-        if (lane == 0) TL(6, 4);
-        named_bar_arrive(kBarT, nc + kWarp);  // consumers may size stage 3 now
-        const int total = run;
-        // balanced share: ranks c, c+G, c+2G, ... of the concatenated rest lists
-        for (int base = blockIdx.x; base < total; base += kWarp * G) {
-            const int my = base + lane * G;
-            int32_t my_i = 0;
-            uint32_t my_b = 0;
-            if (my < total) {
-                int lo = 0, hi = G;  // owner o: pre[o] <= my < pre[o + 1]
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (pre[mid] <= my) lo = mid; else hi = mid;
-                }
-                const uint32_t wv = await_relaxed(S.t_list + (int64_t)lo * rows_per_cta + (my - pre[lo]), tag);
-                my_i = static_cast<int32_t>(wv & ((1u << 27) - 1u));
-                my_b = wv >> 27;
-            }
-            const int n = min(kWarp, (total - base + G - 1) / G);
-            for (int k = 0; k < n; ++k) {
-                const int32_t i = __shfl_sync(0xffffffffu, my_i, k);
-                const uint32_t bits = __shfl_sync(0xffffffffu, my_b, k);
-                if (lane == 0) issue(i, bits);
-                __syncwarp();
-            }
+        int base = 0;
+        if (lane == 0) {
+            red_add_u32(qc + 3, static_cast<unsigned>(n_own));
+            if (ovf > 0) base = static_cast<int>(atomicAdd(qc + 0, static_cast<unsigned>(ovf)));
         }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int k = lane; k < ovf; k += kWarp) {
+            const int32_t i = own_idx[kept + k];
+            st_relaxed_u64(S.t_list + base + k, tagged(tag, static_cast<uint32_t>(i) | (own_bits[kept + k] << 27)));
+            bulk_prefetch_l2(REC + (int64_t)i * L.rs, static_cast<uint32_t>(rec_bytes));  // for its stealer
+        }
+        __syncwarp();
+        if (lane == 0) {
+            red_add_u32(qc + 2, 1u);  // pushed (stealers check each entry's tag, no ordering needed)
+            TL(6, 6);
+            for (; e < kept; ++e) issue(own_idx[e], own_bits[e]);
+            // steal: claim queue slots until every CTA has pushed and the claim is past the tail
+            const unsigned G_u = static_cast<unsigned>(G);
+            for (;;) {
+                const unsigned slot = atomicAdd(qc + 1, 1u);
+                bool got = false;
+                uint32_t wv = 0;
+                for (;;) {
+                    if (slot < static_cast<unsigned>(L.F)) {
+                        const unsigned long long w = ld_relaxed_u64(S.t_list + slot);
+                        if (static_cast<uint32_t>(w >> 32) == tag) {
+                            wv = static_cast<uint32_t>(w);
+                            got = true;
+                            break;
+                        }
+                    }
+                    if (ld_relaxed_u32(qc + 2) == G_u && slot >= ld_relaxed_u32(qc + 0)) break;
+                }
+                if (!got) break;
+                issue(static_cast<int32_t>(wv & ((1u << 27) - 1u)), wv >> 27);
+            }
+            // end-of-work sentinel for the consumers (completes the slot's phase, no bytes)
+            mbar_wait(&empty[st], ph ^ 1);
+            meta[st].idx = -1;
+            mbar_arrive(&full[st]);
+            TL(6, 4);
+        }
+        __syncwarp();
     } else {
         // ================================================================ consumer warps
         const int ct = threadIdx.x;
@@ -283,12 +286,25 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
         pdl_wait();  // y and the scratch words of the previous step are now safe to touch
         if (threadIdx.x == 0) {
             TL(5, 1);
-            cnt[NB + 1] = static_cast<int>(static_cast<uint32_t>(__ldcg(S.ctl + kCtlEpoch)) + 1u);
+            const uint32_t t = static_cast<uint32_t>(__ldcg(S.ctl + kCtlEpoch)) + 1u;
+            cnt[NB + 1] = static_cast<int>(t);
+            // own-work cap: the previous launch's active count spread over the grid (the first
+            // launch keeps everything); queue counters of the NEXT launch are reset here (the
+            // launch that used them last has completed)
+            const unsigned prev = __ldcg(S.ctl + kCtlQueue + ((t + 2u) % 3u) * 32u + 3);
+            cnt[NB + 2] = prev > 0 ? static_cast<int>((prev + G - 1) / G) : (1 << 30);
+            if (blockIdx.x == 0) {
+                unsigned* nq = S.ctl + kCtlQueue + ((t + 1u) % 3u) * 32u;
+                nq[0] = 0u; nq[1] = 0u; nq[2] = 0u; nq[3] = 0u;
+            }
         }
         if (blockIdx.x == G - 1) {
             for (int64_t i = ct; i < (int64_t)nb * L.d; i += nc) y[i] = 0.0f;
             named_bar_sync(kBarC, nc);
-            if (threadIdx.x == 0) __threadfence();  // ordered before this CTA's count word
+            if (threadIdx.x == 0) {
+                __threadfence();  // the zeroed y before the flag every CTA acquires before its reductions
+                st_relaxed_u64(S.t_count + kYZeroWord, tagged(static_cast<uint32_t>(cnt[NB + 1]), 1u));
+            }
         }
         named_bar_sync(kBarC, nc);
         const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
@@ -317,6 +333,13 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
         if (nq > 0) {
             mbar_wait(bar_a, 0);
             if (threadIdx.x == 0) TL(6, 3);
+#ifdef CD_TIMELINE
+            long long ck[6];
+            ck[0] = clock64();
+#define CKS(i) ck[i] = clock64()
+#else
+#define CKS(i) ((void)0)
+#endif
             constexpr int kQ = 4;
             for (int qb = 0; qb < nq; qb += kQ) {
                 float v[kQ * NB];
@@ -343,9 +366,12 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
                     for (int b = 0; b < NB; ++b) v[qq * NB + b] = a0[b] + a1[b];
                 }
                 constexpr int kV = kQ * NB;
+                CKS(1);
                 const float tot = warp_transpose_sum<kV>(v);
                 if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
+                CKS(2);
                 named_bar_sync(kBarC, nc);
+                CKS(3);
                 if (warp == 0 && lane < kV) {
                     const int qq = lane / NB, b = lane % NB;
                     float s = 0.0f;
@@ -353,8 +379,15 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
                     if (qb + qq < nq && b < nb)
                         st_relaxed_u64(S.t_lat + b * L.ldr + q0 + qb + qq, tagged(tag, __float_as_uint(s)));
                 }
+                CKS(4);
                 named_bar_sync(kBarC, nc);
+                CKS(5);
             }
+#ifdef CD_TIMELINE
+            if (threadIdx.x == 0 && blockIdx.x < kTlCtas)
+                for (int i = 0; i < 5; ++i) g_timeline[7][blockIdx.x][i] = static_cast<unsigned long long>(ck[i + 1] - ck[i]);
+#endif
+#undef CKS
         }
         if (threadIdx.x == 0) TL(5, 2);
 
@@ -544,22 +577,14 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
         }
         named_bar_sync(kBarC, nc);
         if (threadIdx.x == 0) TL(5, 4);
-        const int n_own = cnt[0];
-        const int kept = min(n_own, keep0);
-        named_bar_arrive(kBarK, nc + kWarp);  // producer may stream the kept neurons now
-        // publish the rest list, its length and the per-sample alive counts (tagged words)
-        for (int e = kept + ct; e < n_own; e += nc)
-            st_relaxed_u64(S.t_list + c0 + e - kept,
-                           tagged(tag, static_cast<uint32_t>(own_idx[e]) | (own_bits[e] << 27)));
+        named_bar_arrive(kBarK, nc + kWarp);  // producer may schedule stage 3 now
         if (threadIdx.x == 0) {
-            for (int b = 0; b < NB; ++b)
+            st_relaxed_u64(S.t_alive + blockIdx.x * kMaxBatchFast, tagged(tag, static_cast<uint32_t>(cnt[1])));
+            for (int b = 1; b < NB; ++b)
                 st_relaxed_u64(S.t_alive + blockIdx.x * kMaxBatchFast + b, tagged(tag, static_cast<uint32_t>(cnt[1 + b])));
-            st_relaxed_u64(S.t_count + blockIdx.x, tagged(tag, static_cast<uint32_t>(n_own - kept)));
+            (void)await_acquire(S.t_count + kYZeroWord, tag);  // y zeroed (set long ago: one round trip)
+            TL(5, 5);
         }
-        named_bar_sync(kBarT, nc + kWarp);
-        if (threadIdx.x == 0) TL(5, 5);
-        const int total = pre[G];
-        const int n_rec = kept + (total > (int)blockIdx.x ? (total - (int)blockIdx.x + G - 1) / G : 0);
         int st = 0;
         uint32_t ph = 0;
 
@@ -572,8 +597,9 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
 #pragma unroll
                 for (int k = 0; k < 8; ++k) yr[b][j][k] = 0.0f;
         const int64_t row_bytes = L.ld * (int64_t)sizeof(W);
-        for (int g0 = 0; g0 < n_rec; g0 += kGroupF) {
-            const int ns = min(kGroupF, n_rec - g0);
+        int n_rec = 0;  // records consumed (until the producer's sentinel)
+        for (bool done = false; !done;) {
+            int ns = 0;
             constexpr int kV = kGroupF * 2 * NB;
             int sts[kGroupF];
             float v[kV];
@@ -583,15 +609,29 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
                 float g0v[NB], g1v[NB], u0[NB], u1[NB];
 #pragma unroll
                 for (int b = 0; b < NB; ++b) g0v[b] = g1v[b] = u0[b] = u1[b] = 0.0f;
-                if (q < ns) {
+                if (!done) {
                     mbar_wait(&full[st], ph);
+                    if (meta[st].idx < 0) done = true;
+                }
+                if (!done) {
+                    ns = q + 1;
+#ifdef CD_TIMELINE
+                    if (threadIdx.x == 0 && blockIdx.x < kTlCtas) {
+                        const int rec = n_rec + q;
+                        if (rec == 0) TL(4, 0);
+                        if (rec == 3) TL(4, 1);
+                        if (rec == 6) TL(4, 2);
+                        TL(4, 3);
+                        g_timeline[4][blockIdx.x][7] = rec + 1;
+                    }
+#endif
                     const uint8_t* sb = ring + st * stage_bytes;
                     const W* rup = reinterpret_cast<const W*>(sb);
                     const W* rgate = reinterpret_cast<const W*>(sb + row_bytes);
 #pragma unroll
                     for (int j = 0; j < VPT; ++j) {
                         const int vec = ct + j * nc;
-                        if (vec < nvec) {
+                        if (vec < nvec && P.keep0 != -1) {
                             float wg[8], wu[8];
                             Vec8<W>::load(rgate + vec * kVec, wg);
                             Vec8<W>::load(rup + vec * kVec, wu);
@@ -612,6 +652,8 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
                     v[(q * 2 + 1) * NB + b] = u0[b] + u1[b];
                 }
             }
+            if (ns == 0) break;
+            n_rec += ns;
             const float tot = warp_transpose_sum<kV>(v);
             if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
             named_bar_sync(kBarC, nc);
@@ -640,7 +682,7 @@ __global__ void __launch_bounds__(288, 1) k_dc_fused(const __grid_constant__ Fus
 #pragma unroll
                     for (int j = 0; j < VPT; ++j) {
                         const int vec = ct + j * nc;
-                        if (vec < nvec) {
+                        if (vec < nvec && P.keep0 != -1) {
                             float wd[8];
                             Vec8<W>::load(rdown + vec * kVec, wd);
 #pragma unroll
@@ -722,13 +764,14 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
                             const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
                             int* alive_out, const LaunchCfg& c, int keep0) {
     if (!L.theta_at || !S.t_lat || !S.t_list || !S.t_count || !S.t_alive || !S.ctl) return cudaErrorInvalidValue;
-    if (c.num_sms > kMaxCtas || L.F >= (1 << 27)) return cudaErrorInvalidValue;
+    if (c.num_sms >= kYZeroWord || L.F >= (1 << 27)) return cudaErrorInvalidValue;
     // x rows are staged by the TMA engine: 16-byte aligned rows of a multiple of 16 bytes
     if (L.d % 4 != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0) return cudaErrorInvalidValue;
     const int64_t nvec = L.ld / kVec;
+    // consumer threads own vpt 8-element column vectors each: up to 16 consumer warps
     int vpt = 0;
     for (int v : {1, 2, 4})
-        if ((nvec + v - 1) / v <= 256) { vpt = v; break; }
+        if ((nvec + v - 1) / v <= kMaxConsumers) { vpt = v; break; }
     if (vpt == 0) return cudaErrorInvalidValue;
     const int nvr = static_cast<int>(L.ldr / kVec);
     const int vpl = nvr <= 32 ? 1 : nvr <= 64 ? 2 : nvr <= 128 ? 4 : 0;
@@ -744,13 +787,13 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     const int64_t esz = L.dtype == kBF16 ? 2 : 4;
     const int64_t stage_bytes = 3 * L.ld * esz;
     const int64_t brow_bytes = mma ? L.kst * 32 : L.ldr * esz;
-    const int threads = 288;
-    const int nwc = threads / kWarp - 1;
+    const int nwc = static_cast<int>(std::max<int64_t>(8, ((nvec + vpt - 1) / vpt + kWarp - 1) / kWarp));
+    const int threads = (nwc + 1) * kWarp;
     // fixed carve-up beside the ring: latent, barriers, meta, lists, scratch, latent fragments
     // (the theta_at slice is overlaid on the ring's tail)
     const int64_t aux_bytes = (int64_t)qrows * L.ld * esz;
     const int64_t fixed = (int64_t)nbk * L.ldr * 4 + 3 * 8 + (int64_t)rpc * 8 + (nwc * 32 + kGroupF * nbk) * 4 +
-                          (2 + nbk) * 4 + (int64_t)(G + 1) * 4 + 16 + (mma ? L.kst * 256 : 0) + 64;
+                          (3 + nbk) * 4 + 16 + (mma ? L.kst * 256 : 0) + 64;
     const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
     const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
     if (nstages < 2) return cudaErrorInvalidValue;

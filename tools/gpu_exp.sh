@@ -1,4 +1,3 @@
-for k in 0 3 6; do
-  echo "=== keep0=$k"
-  CD_KEEP0=$k timeout 120 python tools/timeline.py dc 0.9 2>&1 | tail -4
-done
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+CD_LIB_DIR=_lib_tl timeout 120 python tools/timeline.py dc 0.9 2>&1 | sed -n 1,8p
+for i in 1 2; do timeout 300 python bench.py --no-cpu-baseline --no-sweep --steps 400 2>&1 | tail -1 | cut -c1-200; done

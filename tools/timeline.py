@@ -13,7 +13,7 @@ import paper_2505_17701_b200 as cd  # noqa: E402
 from paper_2505_17701_b200 import _capi  # noqa: E402
 
 K, CT, P = 8, 160, 8
-NAMES = {0: "latent", 1: "ind_dc", 2: "sparse_dc", 3: "sparse_mc", 4: "ind_mc", 5: "dc_fused", 6: "fused_st2", 7: "fused_prod"}
+NAMES = {0: "latent", 1: "ind_dc", 2: "sparse_dc", 3: "sparse_mc", 4: "st3_recs", 5: "dc_fused", 6: "fused_st2", 7: "fused_prod"}
 
 
 def read():
@@ -29,6 +29,15 @@ def show(tl, label):
     s2 = tl[7, :148, 6].copy()
     tl[7, :, 7] = 0
     tl[7, :, 6] = 0
+    c1 = tl[7, :148, 0:5].copy()
+    tl[7, :, 0:5] = 0
+    if (c1 > 0).any():
+        m = np.median(c1[c1[:, 0] > 0], axis=0)
+        print("    stage-1 cycles (thread 0): compute %d, transpose %d, bar %d, final+store %d, bar %d" % tuple(m))
+    nrec = tl[4, :148, 7].copy()
+    tl[4, :, 7] = 0
+    if (nrec > 0).any():
+        print(f"    stage-3 records per CTA: min {nrec.min()} median {np.median(nrec):.0f} max {nrec.max()}")
     if (s2 > 0).any():
         print(f"    stage-2 loop cycles (thread 0): median {np.median(s2[s2 > 0]):.0f}, max {s2.max():.0f}")
     if (cyc > 0).any():

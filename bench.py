@@ -124,6 +124,18 @@ def workload():
     return layer, pred, xcal, xs
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu summary
+    (profiles/ncu_traffic.json, written from a `ncu --set full` capture), else None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        j = json.load(f)
+    v = j.get(kernel)
+    return None if v is None else float(v["dram_bytes_per_launch"])
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -428,7 +440,7 @@ def run_ours(args):
                                 "PDL-chained" + (", + NCCL all-reduce" if world > 1 else "") + ")"},
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": None, "alg_bytes_per_launch": stage_bytes[dom],
+                         "traffic": ncu_traffic(names[dom]), "alg_bytes_per_launch": stage_bytes[dom],
                          "stages": stages,
                          "step": {"alg_bytes": bytes_step, "gbs": round(bytes_step / (1e6 * ms / args.steps), 1),
                                   "frac": round(bytes_step / (1e6 * ms / args.steps) / peak, 4)}},

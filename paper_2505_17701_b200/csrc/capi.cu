@@ -482,12 +482,7 @@ int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, co
             e = cudaMemcpyAsync(tmp, theta_b, sizeof(float) * d_rank * h->F_total, cudaMemcpyHostToDevice, h->stream);
         if (e == cudaSuccess)
             e = cdk::launch_pack_transpose(tmp, d_rank, h->F_total, h->row_begin, L.F, tbt, L.dtype, ldr, h->stream);
-        void* tfrag = nullptr;
-        const int64_t kst = (d_rank + 15) / 16;
-        if (e == cudaSuccess && L.dtype == CD_DTYPE_BF16) {
-            tfrag = h->dalloc<uint8_t>(static_cast<size_t>((L.F + 15) / 16 * kst * 512), false);
-            e = cdk::launch_pack_frag_bt(tmp, d_rank, h->F_total, h->row_begin, L.F, tfrag, h->stream);
-        }
+
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         cudaFree(tmp);
         ck(e, "predictor upload");
@@ -499,8 +494,6 @@ int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, co
         L.theta_a = ta;
         L.theta_at = tat;
         L.theta_bt = tbt;
-        L.theta_bt_frag = tfrag;
-        L.kst = kst;
     });
 }
 

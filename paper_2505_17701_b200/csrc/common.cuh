@@ -110,25 +110,6 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float b0, float b1, 
         : "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
 
-// Warp-level bf16 tensor-core MMA, D(16x8, f32) += A(16x16, row) * B(16x8, col).  Fragment
-// layout (lane = 4g + t): a0 = A[g][2t..2t+1], a1 = A[g+8][2t..], a2 = A[g][2t+8..],
-// a3 = A[g+8][2t+8..]; b0 = B[2t..2t+1][g], b1 = B[2t+8..2t+9][g]; d0,d1 = D[g][2t..2t+1],
-// d2,d3 = D[g+8][2t..2t+1].  Used for the predictor GEMV of the fused decode kernel, where it
-// removes the bf16 unpack + FMA instruction stream (the stage is latency-, not FLOP-bound).
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint4& a, const uint2& b) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
-        "{%8, %9}, {%0, %1, %2, %3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y));
-}
-
-// Two floats -> bf16x2 (RNE), the first in the low half.
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<const uint32_t*>(&v);
-}
-
 // ---------------------------------------------------------------- global reductions
 // red.global.add.v4.f32 (sm_90+): one vector reduction instead of four scalar atomics.
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -205,6 +186,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+
+// Bulk reduction shared -> global by the TMA engine: dst[i] += src[i] (f32), whole lines at L2.
+// dst, src 16-byte aligned, bytes a multiple of 16.  Completion tracked by a bulk group.
+__device__ __forceinline__ void bulk_reduce_add_f32(float* dst, const float* src, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+
+// Commit this thread's bulk group and wait until its shared-memory SOURCES have been read (the
+// global side completes asynchronously; kernel completion publishes it).
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// Order this thread's generic-proxy shared-memory writes before later async-proxy (TMA) reads.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Bulk prefetch global -> L2 (the TMA engine; no shared memory, no completion to wait for).

@@ -38,11 +38,6 @@ struct LayerDev {
     const void* theta_a = nullptr;   // d x ldr
     const void* theta_at = nullptr;  // r x ld  (theta_a transposed: one latent column per row)
     const void* theta_bt = nullptr;  // F x ldr
-    // bf16 layers: theta_bt re-arranged in mma.sync m16n8k16 A-fragment order, tile by tile:
-    // tile T (rows 16T..16T+15) x k-step s (columns 16s..16s+15) is 512 contiguous bytes,
-    // lane l's 16 bytes = its {a0, a1, a2, a3} (zero-padded past F and r).  kst = ceil(r/16).
-    const void* theta_bt_frag = nullptr;
-    int64_t kst = 0;
 };
 
 // Per-handle device scratch.  latent/count/done are "self-cleaning": every kernel
@@ -142,9 +137,6 @@ cudaError_t read_timeline_fused(unsigned long long* out, int64_t n);
 // dst row r = src row r (cols values, zero-padded to ld_pad), rows ld_dst apart.
 cudaError_t launch_pack_rows(const float* src, int64_t rows, int64_t cols, int64_t ld_src,
                              void* dst, int dtype, int64_t ld_pad, int64_t ld_dst, cudaStream_t s);
-// theta_bt_frag (see LayerDev) from the f32 theta_b (r x ld_src), columns [col_begin, +F).
-cudaError_t launch_pack_frag_bt(const float* theta_b, int64_t r, int64_t ld_src, int64_t col_begin,
-                                int64_t F, void* dst, cudaStream_t s);
 // dst (cols_sel x ldr) = transpose of src[:, col_begin:col_begin+cols_sel] (src rows x ld_src).
 cudaError_t launch_pack_transpose(const float* src, int64_t rows, int64_t ld_src,
                                   int64_t col_begin, int64_t cols_sel, void* dst, int dtype,

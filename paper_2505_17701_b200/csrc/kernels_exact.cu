@@ -240,42 +240,9 @@ __global__ void k_pack_transpose(const float* __restrict__ src, int64_t rows, in
     }
 }
 
-// theta_bt in mma A-fragment order: output word w = ((T * kst + s) * 32 + lane) * 4 + j holds
-// A[row][k], A[row][k+1] with row = 16T + g + (j & 1) * 8, k = 16s + 2t + (j >> 1) * 8,
-// A[row][k] = theta_b[k][col_begin + row] (zero past F or r).
-__global__ void k_pack_frag_bt(const float* __restrict__ tb, int64_t r, int64_t ld_src, int64_t col_begin,
-                               int64_t F, int64_t kst, uint32_t* __restrict__ dst, int64_t nwords) {
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
-         w += (int64_t)gridDim.x * blockDim.x) {
-        const int j = static_cast<int>(w & 3);
-        const int lane = static_cast<int>((w >> 2) & 31);
-        const int64_t ts = w >> 7;
-        const int64_t s = ts % kst, T = ts / kst;
-        const int g = lane >> 2, t = lane & 3;
-        const int64_t row = 16 * T + g + (j & 1) * 8;
-        const int64_t k = 16 * s + 2 * t + (j >> 1) * 8;
-        float v0 = 0.0f, v1 = 0.0f;
-        if (row < F) {
-            if (k < r) v0 = tb[k * ld_src + col_begin + row];
-            if (k + 1 < r) v1 = tb[(k + 1) * ld_src + col_begin + row];
-        }
-        const __nv_bfloat162 p = __floats2bfloat162_rn(v0, v1);
-        dst[w] = *reinterpret_cast<const uint32_t*>(&p);
-    }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_pack_frag_bt(const float* theta_b, int64_t r, int64_t ld_src, int64_t col_begin,
-                                int64_t F, void* dst, cudaStream_t s) {
-    const int64_t kst = (r + 15) / 16, tiles = (F + 15) / 16;
-    const int64_t nwords = tiles * kst * 128;
-    const int blocks = static_cast<int>(imin64(4096, (nwords + 255) / 256));
-    k_pack_frag_bt<<<blocks, 256, 0, s>>>(theta_b, r, ld_src, col_begin, F, kst, static_cast<uint32_t*>(dst), nwords);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_compact_masks(const LayerDev& L, const Scratch& S, const uint8_t* masks,
                                  const float* u_full, int nb, float* y, const LaunchCfg& c) {
     return launch_ex(k_compact, dim3(1), dim3(1024), 0, c, false, L, S, masks ? 2 : 3,

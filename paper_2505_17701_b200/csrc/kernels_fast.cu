@@ -279,7 +279,7 @@ __global__ void k_indicator_dc(LayerDev L, Scratch S, int nb, int rows_per_cta, 
 constexpr int kSR = 4;
 
 template <typename W, int NB, int VPT, bool kCats>
-__global__ void k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __restrict__ x,
+__global__ void __launch_bounds__(416, 1) k_indicator_mc(LayerDev L, Scratch S, int nb, const float* __restrict__ x,
                                int rows_per_cta, int nstages, float tau, float* __restrict__ y,
                                int64_t y_len, uint8_t* __restrict__ mask_out,
                                float* __restrict__ u_out) {
@@ -462,7 +462,7 @@ struct SlotMeta {
 //       kCATS s = (W_up[i].x) h_i (h = act(gate) from the list) copies [up|gate|down] (the gate
 //             row rides along unused: CATS is a comparison baseline, not the hot path)
 template <typename W, int NB, int VPT, int KIND>
-__global__ void k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict__ x, int nstages,
+__global__ void __launch_bounds__(416, 1) k_sparse(LayerDev L, Scratch S, int nb, const float* __restrict__ x, int nstages,
                          bool dense, float* __restrict__ y, int* __restrict__ alive_out) {
     constexpr bool kMC = KIND == kMC_;
     constexpr bool kOneDot = KIND != kDC_;    // one dot product per neuron (MC, CATS)

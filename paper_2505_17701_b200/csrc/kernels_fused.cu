@@ -80,6 +80,16 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// A 16-byte streaming load the compiler may not sink towards its use (volatile asm keeps it
+// ahead of griddepcontrol.wait, so its DRAM latency overlaps the previous grid's tail).
+__device__ __forceinline__ uint4 ldg_early_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long tagged(uint32_t tag, uint32_t payload) {
     return (static_cast<unsigned long long>(tag) << 32) | payload;
 }
@@ -121,8 +131,10 @@ struct FusedParams {
 
 template <typename W, int NB, int VPT, int VPL>
 __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ FusedParams P) {
-    // bf16 layers run the predictor GEMV on the tensor cores (theta_bt in A-fragment order)
-    constexpr bool kMma = std::is_same<W, __nv_bfloat16>::value;
+    // bf16 layers keep the CTA's predictor rows in REGISTERS, loaded before griddepcontrol.wait
+    // (the stage is then pure FFMA once the latent arrives); f32 layers stage them through smem
+    constexpr bool kRegB = std::is_same<W, __nv_bfloat16>::value;
+    constexpr int kRowsW = 8;  // predictor rows per consumer warp (register path)
     const LayerDev& L = P.L;
     const Scratch& S = P.S;
     const int nb = P.nb, nstages = P.nstages, rows_per_cta = P.rows_per_cta, qrows = P.qrows;
@@ -145,8 +157,7 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
     const int G = gridDim.x;
     const int64_t rec_bytes = 3 * L.ld * (int64_t)sizeof(W);   // one neuron record
     const int64_t stage_bytes = rec_bytes;
-    // one predictor row in the chunk: ldr elements (f32 row layout) or kst*16 (fragment layout)
-    const int64_t brow_bytes = kMma ? L.kst * 32 : L.ldr * (int64_t)sizeof(W);
+    const int64_t brow_bytes = L.ldr * (int64_t)sizeof(W);     // one predictor row
     const int64_t arow_bytes = L.ld * (int64_t)sizeof(W);      // one theta_at row
 
     // ---- shared memory carve-up (all offsets multiples of 16).  The theta_at slice and x live
@@ -166,8 +177,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
     float* red = reinterpret_cast<float*>(own_bits + rows_per_cta);  // [nwc][32] warp partials
     float* sval = red + nwc * 32;                                      // [kGroupF * NB]
     int* cnt = reinterpret_cast<int*>(sval + kGroupF * NB);  // [0] n_own [1..NB] alive [NB+1] tag [NB+2] cap
-    uint2* latfrag = reinterpret_cast<uint2*>(
-        (reinterpret_cast<uintptr_t>(cnt + NB + 3) + 15) & ~static_cast<uintptr_t>(15));  // [kst][32] B fragments
 
     const int64_t c0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t c1 = imin64(L.F, c0 + rows_per_cta);
@@ -191,7 +200,7 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
     __syncthreads();
     pdl_launch_dependents();
 
-    const uint8_t* BT = static_cast<const uint8_t*>(kMma ? L.theta_bt_frag : L.theta_bt);
+    const uint8_t* BT = static_cast<const uint8_t*>(L.theta_bt);
     const W* AT = static_cast<const W*>(L.theta_at);
     const W* REC = static_cast<const W*>(L.w_up);   // records [up | gate | down], stride L.rs
 
@@ -206,9 +215,8 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
                 mbar_arrive_expect_tx(bar_a, static_cast<uint32_t>(nq * arow_bytes));
                 bulk_g2s(abuf, AT + (int64_t)q0 * L.ld, static_cast<uint32_t>(nq * arow_bytes), bar_a, pol);
             }
-            if (nrows > 0) {
-                // rows_per_cta is a multiple of 16 in the fragment layout: whole tiles
-                const int64_t bytes = kMma ? (nrows + 15) / 16 * 16 * brow_bytes : nrows * brow_bytes;
+            if (!kRegB && nrows > 0) {
+                const int64_t bytes = nrows * brow_bytes;
                 mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bytes));
                 bulk_g2s(ring, BT + c0 * brow_bytes, static_cast<uint32_t>(bytes), bar_b, pol);
             }
@@ -283,6 +291,23 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         // ================================================================ consumer warps
         const int ct = threadIdx.x;
         const int nvec = static_cast<int>(L.ld / kVec);
+        const int nvr = static_cast<int>(L.ldr / kVec);
+        // register path: this warp's predictor rows (warp + i*nwc of the chunk), lane owns
+        // vectors lane + v*32 of each row -- coalesced 16-byte loads, weights only
+        uint4 rb[kRegB ? kRowsW : 1][VPL];
+        if constexpr (kRegB) {
+            const W* BTw = static_cast<const W*>(L.theta_bt);
+#pragma unroll
+            for (int i = 0; i < kRowsW; ++i) {
+                const int rl = warp + i * nwc;
+#pragma unroll
+                for (int v = 0; v < VPL; ++v) {
+                    const int vec = lane + v * kWarp;
+                    rb[i][v] = make_uint4(0u, 0u, 0u, 0u);
+                    if (rl < nrows && vec < nvr) rb[i][v] = ldg_early_v4(BTw + (c0 + rl) * L.ldr + vec * kVec);
+                }
+            }
+        }
         pdl_wait();  // y and the scratch words of the previous step are now safe to touch
         if (threadIdx.x == 0) {
             TL(5, 1);
@@ -415,84 +440,83 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
 #ifdef CD_TIMELINE
         long long clk_s2 = 0;
 #endif
-        if constexpr (kMma) {
-            // B fragments of the latent: column g of the 16x8 B tile is sample g/2, split into a
-            // bf16 high part (g even) and the bf16 of the remainder (g odd): ~16-bit precision
-            for (int e = ct; e < L.kst * 32; e += nc) {
-                const int s = e >> 5, l = e & 31, g = l >> 2, t = l & 3;
-                uint2 v = make_uint2(0u, 0u);
-                if (g < 2 * NB) {
-                    const int b = g >> 1;
-                    const int k = 16 * s + 2 * t;
-                    float f[4];
+        if constexpr (kRegB) {
+            float lat[NB][VPL][8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int kk = k + (u & 1) + (u >> 1) * 8;
-                        const float val = kk < L.r ? latbuf[b * L.ldr + kk] : 0.0f;
-                        const float hiv = __bfloat162float(__float2bfloat16_rn(val));
-                        f[u] = (g & 1) ? val - hiv : hiv;
+            for (int v = 0; v < VPL; ++v) {
+                const int vec = lane + v * kWarp;
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+                    if (vec < nvr) {
+                        const float4* src = reinterpret_cast<const float4*>(latbuf + b * L.ldr + vec * kVec);
+                        lo = src[0];
+                        hi = src[1];
                     }
-                    v.x = pack_bf16x2(f[0], f[1]);
-                    v.y = pack_bf16x2(f[2], f[3]);
+                    lat[b][v][0] = lo.x; lat[b][v][1] = lo.y; lat[b][v][2] = lo.z; lat[b][v][3] = lo.w;
+                    lat[b][v][4] = hi.x; lat[b][v][5] = hi.y; lat[b][v][6] = hi.z; lat[b][v][7] = hi.w;
                 }
-                latfrag[e] = v;
             }
-            named_bar_sync(kBarC, nc);
-            if (nrows > 0) mbar_wait(bar_b, 0);
             if (threadIdx.x == 0) TL(6, 0);
 #ifdef CD_TIMELINE
             clk_s2 = clock64();
 #endif
-            const int g = lane >> 2, t = lane & 3;
-            const int ntile = (nrows + 15) / 16;
-            for (int tt = warp; tt < ntile; tt += nwc) {
-                float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
-                const uint4* A = reinterpret_cast<const uint4*>(ring + (int64_t)tt * L.kst * 512) + lane;
-                const uint2* B = latfrag + lane;
-                int s = 0;
-#pragma unroll 4
-                for (; s + 1 < L.kst; s += 2) {
-                    mma_bf16_16816(acc0, A[s * 32], B[s * 32]);
-                    mma_bf16_16816(acc1, A[(s + 1) * 32], B[(s + 1) * 32]);
-                }
-                if (s < L.kst) mma_bf16_16816(acc0, A[s * 32], B[s * 32]);
-                // lane (g, t): rows g and g+8 of the tile, sample t (its hi + lo columns)
+            constexpr int kV = kRowsW * NB;
+            float v[kV];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const float z = h ? (acc0[2] + acc0[3]) + (acc1[2] + acc1[3])
-                                      : (acc0[0] + acc0[1]) + (acc1[0] + acc1[1]);
-                    const int rl = tt * 16 + g + 8 * h;
-                    const bool valid = rl < nrows;
-                    const int64_t gi = c0 + rl;
-                    bool a = false;
-                    if (valid && t < nb) {
-                        a = ovr ? (ovr[t * L.F + gi] != 0) : (z > tau);
-                        if (mask_out) mask_out[t * L.F + gi] = a ? 1 : 0;
-                        if (logits_out) logits_out[t * L.F + gi] = z;
-                    }
-                    uint32_t bits = static_cast<uint32_t>(a) << t;
-                    bits |= __shfl_xor_sync(0xffffffffu, bits, 1);
-                    bits |= __shfl_xor_sync(0xffffffffu, bits, 2);
+            for (int i = 0; i < kRowsW; ++i) {
+                float a0[NB], a1[NB];
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) {
-                        const unsigned bal = __ballot_sync(0xffffffffu, a && t == b);
-                        if (lane == 0 && bal) atomicAdd(&cnt[1 + b], __popc(bal));
+                for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0f;
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) {
+                    float w[8];
+                    const uint32_t raw[4] = {rb[i][q].x, rb[i][q].y, rb[i][q].z, rb[i][q].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        w[2 * k] = __uint_as_float(raw[k] << 16);
+                        w[2 * k + 1] = __uint_as_float(raw[k] & 0xffff0000u);
                     }
-                    const bool take = t == 0 && bits != 0;
-                    const unsigned any = __ballot_sync(0xffffffffu, take);
-                    int e0 = 0;
-                    if (lane == 0 && any) e0 = atomicAdd(&cnt[0], __popc(any));
-                    e0 = __shfl_sync(0xffffffffu, e0, 0);
-                    if (take) {
-                        const int e = e0 + __popc(any & ((1u << lane) - 1u));
-                        own_idx[e] = static_cast<int32_t>(gi);
-                        own_bits[e] = bits;
-                    }
+#pragma unroll
+                    for (int b = 0; b < NB; ++b)
+#pragma unroll
+                        for (int k = 0; k < 8; k += 2) ffma2(a0[b], a1[b], w[k], w[k + 1], lat[b][q][k], lat[b][q][k + 1]);
                 }
+#pragma unroll
+                for (int b = 0; b < NB; ++b) v[i * NB + b] = a0[b] + a1[b];
+            }
+            const float tot = warp_transpose_sum<kV>(v);
+            if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
+            __syncwarp();
+            // lanes 0..kRowsW-1: row warp + lane*nwc of the chunk
+            const int rl = warp + lane * nwc;
+            const bool valid = lane < kRowsW && rl < nrows;
+            const int64_t gi = c0 + rl;
+            uint32_t bits = 0;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                bool a = false;
+                if (valid && b < nb) {
+                    const float z = red[warp * 32 + lane * NB + b];
+                    a = ovr ? (ovr[b * L.F + gi] != 0) : (z > tau);
+                    if (mask_out) mask_out[b * L.F + gi] = a ? 1 : 0;
+                    if (logits_out) logits_out[b * L.F + gi] = z;
+                }
+                bits |= static_cast<uint32_t>(a) << b;
+                const unsigned bal = __ballot_sync(0xffffffffu, a);
+                if (lane == 0 && bal) atomicAdd(&cnt[1 + b], __popc(bal));
+            }
+            const unsigned any = __ballot_sync(0xffffffffu, bits != 0);
+            int e0 = 0;
+            if (lane == 0 && any) e0 = atomicAdd(&cnt[0], __popc(any));
+            e0 = __shfl_sync(0xffffffffu, e0, 0);
+            if (bits) {
+                const int e = e0 + __popc(any & ((1u << lane) - 1u));
+                own_idx[e] = static_cast<int32_t>(gi);
+                own_bits[e] = bits;
             }
         } else {
         float lat[NB][VPL][8];
-        const int nvr = static_cast<int>(L.ldr / kVec);
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
             const int vec = lane + v * kWarp;
@@ -571,7 +595,7 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         if (threadIdx.x == 0) {
             TL(6, 1);
 #ifdef CD_TIMELINE
-            if constexpr (kMma)
+            if constexpr (kRegB)
                 if (blockIdx.x < kTlCtas) g_timeline[7][blockIdx.x][6] = static_cast<unsigned long long>(clock64() - clk_s2);
 #endif
         }
@@ -699,27 +723,28 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         }
         if (threadIdx.x == 0) TL(5, 6);
         if (n_rec > 0) {
+            // this CTA's partial y -> shared memory (the ring is idle now) -> ONE bulk reduction
+            // into global y by the TMA engine (cp.reduce.async.bulk .add.f32): line-granular
+            // adds at L2 instead of 1024 contended red.v4 per CTA, which the next step's
+            // griddepcontrol.wait would otherwise have to drain
+            named_bar_sync(kBarC, nc);  // every consumer is past its last ring read
+            float* ys = reinterpret_cast<float*>(ring);
 #pragma unroll
             for (int j = 0; j < VPT; ++j) {
                 const int vec = ct + j * nc;
-                if (vec < nvec) {
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)
+                for (int b = 0; b < NB; ++b)
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            if (b >= nb) continue;
-                            const int64_t col = (int64_t)vec * kVec + h * 4;
-                            float* dst = y + b * L.d + col;
-                            if (col + 4 <= L.d && ((L.d & 3) == 0)) {
-                                red_add_v4(dst, yr[b][j][h * 4], yr[b][j][h * 4 + 1], yr[b][j][h * 4 + 2],
-                                           yr[b][j][h * 4 + 3]);
-                            } else {
-#pragma unroll
-                                for (int k = 0; k < 4; ++k)
-                                    if (col + k < L.d) red_add_f32(dst + k, yr[b][j][h * 4 + k]);
-                            }
-                        }
-                }
+                    for (int k = 0; k < 8; ++k) {
+                        const int64_t col = (int64_t)vec * kVec + k;
+                        if (b < nb && vec < nvec && col < L.d) ys[b * L.d + col] = yr[b][j][k];
+                    }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(kBarC, nc);
+            if (threadIdx.x == 0) {
+                bulk_reduce_add_f32(y, ys, static_cast<uint32_t>(nb * L.d * sizeof(float)));
+                bulk_commit_and_wait_read();
             }
         }
         if (blockIdx.x == 0 && warp == 0) {
@@ -779,25 +804,25 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     const int nbk = nb <= 1 ? 1 : (nb <= 2 ? 2 : 4);
     if (nbk * kRBf > 32 || nbk * kGroupF * 2 > 32 || nbk * vpt > 8) return cudaErrorInvalidValue;
     const int G = c.num_sms;
-    const bool mma = L.dtype == kBF16;
-    if (mma && (!L.theta_bt_frag || L.kst <= 0)) return cudaErrorInvalidValue;
-    // neuron chunk per CTA: whole 16-row tiles in the fragment layout
-    const int rpc = mma ? static_cast<int>(16 * (((L.F + 15) / 16 + G - 1) / G)) : static_cast<int>((L.F + G - 1) / G);
+    const bool regb = L.dtype == kBF16;
+    const int rpc = static_cast<int>((L.F + G - 1) / G);
     const int qrows = static_cast<int>((L.r + G - 1) / G);
     const int64_t esz = L.dtype == kBF16 ? 2 : 4;
     const int64_t stage_bytes = 3 * L.ld * esz;
-    const int64_t brow_bytes = mma ? L.kst * 32 : L.ldr * esz;
+    const int64_t brow_bytes = L.ldr * esz;
     const int nwc = static_cast<int>(std::max<int64_t>(8, ((nvec + vpt - 1) / vpt + kWarp - 1) / kWarp));
     const int threads = (nwc + 1) * kWarp;
     // fixed carve-up beside the ring: latent, barriers, meta, lists, scratch, latent fragments
     // (the theta_at slice is overlaid on the ring's tail)
     const int64_t aux_bytes = (int64_t)qrows * L.ld * esz;
     const int64_t fixed = (int64_t)nbk * L.ldr * 4 + 3 * 8 + (int64_t)rpc * 8 + (nwc * 32 + kGroupF * nbk) * 4 +
-                          (3 + nbk) * 4 + 16 + (mma ? L.kst * 256 : 0) + 64;
+                          (3 + nbk) * 4 + 64;
     const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
     const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
     if (nstages < 2) return cudaErrorInvalidValue;
-    if ((int64_t)rpc * brow_bytes + aux_bytes > stage_bytes * nstages) return cudaErrorInvalidValue;
+    if (regb ? rpc > nwc * 8 : (int64_t)rpc * brow_bytes + aux_bytes > stage_bytes * nstages)
+        return cudaErrorInvalidValue;  // register path: <= 8 predictor rows per consumer warp
+    if (aux_bytes > stage_bytes * nstages) return cudaErrorInvalidValue;
     const size_t smem = static_cast<size_t>(fixed + per_stage * nstages);
     auto go = [&](auto kern) {
         cudaError_t e = set_smem(kern, smem);

@@ -145,9 +145,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
     uint8_t* __restrict__ mask_out = P.mask_out;
     float* __restrict__ logits_out = P.logits_out;
     if (threadIdx.x == 0) TL(5, 0);
-#ifdef CD_TIMELINE
-    const long long clk0 = clock64();
-#endif
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int kBarC = 1;   // consumers only
     constexpr int kBarK = 3;   // consumers -> producer: own list, counts and launch tag in smem
@@ -358,13 +355,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         if (nq > 0) {
             mbar_wait(bar_a, 0);
             if (threadIdx.x == 0) TL(6, 3);
-#ifdef CD_TIMELINE
-            long long ck[6];
-            ck[0] = clock64();
-#define CKS(i) ck[i] = clock64()
-#else
-#define CKS(i) ((void)0)
-#endif
             constexpr int kQ = 4;
             for (int qb = 0; qb < nq; qb += kQ) {
                 float v[kQ * NB];
@@ -391,12 +381,9 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
                     for (int b = 0; b < NB; ++b) v[qq * NB + b] = a0[b] + a1[b];
                 }
                 constexpr int kV = kQ * NB;
-                CKS(1);
                 const float tot = warp_transpose_sum<kV>(v);
                 if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
-                CKS(2);
                 named_bar_sync(kBarC, nc);
-                CKS(3);
                 if (warp == 0 && lane < kV) {
                     const int qq = lane / NB, b = lane % NB;
                     float s = 0.0f;
@@ -404,15 +391,8 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
                     if (qb + qq < nq && b < nb)
                         st_relaxed_u64(S.t_lat + b * L.ldr + q0 + qb + qq, tagged(tag, __float_as_uint(s)));
                 }
-                CKS(4);
                 named_bar_sync(kBarC, nc);
-                CKS(5);
             }
-#ifdef CD_TIMELINE
-            if (threadIdx.x == 0 && blockIdx.x < kTlCtas)
-                for (int i = 0; i < 5; ++i) g_timeline[7][blockIdx.x][i] = static_cast<unsigned long long>(ck[i + 1] - ck[i]);
-#endif
-#undef CKS
         }
         if (threadIdx.x == 0) TL(5, 2);
 
@@ -437,9 +417,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         }
         named_bar_sync(kBarC, nc);
         if (threadIdx.x == 0) TL(5, 3);
-#ifdef CD_TIMELINE
-        long long clk_s2 = 0;
-#endif
         if constexpr (kRegB) {
             float lat[NB][VPL][8];
 #pragma unroll
@@ -458,9 +435,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
                 }
             }
             if (threadIdx.x == 0) TL(6, 0);
-#ifdef CD_TIMELINE
-            clk_s2 = clock64();
-#endif
             constexpr int kV = kRowsW * NB;
             float v[kV];
 #pragma unroll
@@ -594,10 +568,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         }
         if (threadIdx.x == 0) {
             TL(6, 1);
-#ifdef CD_TIMELINE
-            if constexpr (kRegB)
-                if (blockIdx.x < kTlCtas) g_timeline[7][blockIdx.x][6] = static_cast<unsigned long long>(clock64() - clk_s2);
-#endif
         }
         named_bar_sync(kBarC, nc);
         if (threadIdx.x == 0) TL(5, 4);
@@ -764,9 +734,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
     }
     if (threadIdx.x == 0) {
         TL(5, 7);
-#ifdef CD_TIMELINE
-        if (blockIdx.x < kTlCtas) g_timeline[7][blockIdx.x][7] = static_cast<unsigned long long>(clock64() - clk0);
-#endif
     }
 }
 

@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         for (int k = lane; k < ovf; k += kWarp) {
             const int32_t i = own_idx[kept + k];
             st_relaxed_u64(S.t_list + base + k, tagged(tag, static_cast<uint32_t>(i) | (own_bits[kept + k] << 27)));
-            bulk_prefetch_l2(REC + (int64_t)i * L.rs, static_cast<uint32_t>(rec_bytes));  // for its stealer
+
         }
         __syncwarp();
         if (lane == 0) {

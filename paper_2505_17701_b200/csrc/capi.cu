@@ -180,7 +180,12 @@ int run_chain(cd_layer* h, const Req& r) {
                 ck(cdk::launch_sparse_fast(L, S, cdk::kDC, true, xc, n, yc, ao, c), "dense");
                 launches += 2;
                 mark(0);
+            } else if (r.method == cdk::kMC && n == 1 && h->use_fused &&
+                       cdk::launch_mc_fused(L, S, xc, r.tau, yc, mo, io, ao, c) == cudaSuccess) {
+                launches += 1;
+                mark(0);
             } else if (r.method == cdk::kMC || r.method == cdk::kCATS) {
+                (void)cudaGetLastError();
                 const bool cats = r.method == cdk::kCATS;
                 ck(cdk::launch_indicator_mc_fast(L, S, xc, n, r.tau, yc, mo, io, c, cats), "indicator_mc");
                 mark(0);
@@ -399,6 +404,7 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     S.alive = h->dalloc<int>(kMaxBatch);
     S.ctl = h->dalloc<unsigned>(128);
     S.t_list = h->dalloc<unsigned long long>(L.F);
+    S.t_aux = h->dalloc<unsigned long long>(L.F);
     S.t_count = h->dalloc<unsigned long long>(cdk::kMaxCtas);
     S.t_alive = h->dalloc<unsigned long long>(cdk::kMaxCtas * kMaxBatchFast);
     if (const char* env = std::getenv("CD_DC_CHAIN")) h->use_fused = env[0] != '1';
@@ -794,7 +800,7 @@ int cd_bench_stages(cd_layer* const* hs, int n_handles, int method, int64_t batc
             ck(cdk::launch_spin(30000ull, s), "spin");  // host enqueues the timed work meanwhile
             ck(cudaEventRecord(ev[0], s), "event");
             const int nl = run_chain(h, r);
-            if (method == CD_METHOD_DC) nst = nl;  // 1 when the fused kernel ran, 3 for the chain
+            if (method == CD_METHOD_DC || method == CD_METHOD_MC) nst = nl;  // 1 when a fused kernel ran
             err = cudaEventSynchronize(ev[nst]);
             if (it < warmup) continue;
             for (int k = 0; k < nst && err == cudaSuccess; ++k) {

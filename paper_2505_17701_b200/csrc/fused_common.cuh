@@ -1,0 +1,84 @@
+// fused_common.cuh -- inter-CTA exchange helpers of the persistent fused decode kernels
+// (kernels_fused.cu: D-CountDown, kernels_fused_mc.cu: M-CountDown).
+//
+// CTAs exchange data through EPOCH-TAGGED 64-bit words {payload, launch tag} written with one
+// single-copy-atomic store; readers spin until the tag matches.  No fence sits on the critical
+// path, so no CTA waits for its own in-flight bulk copies (a release fence does).  The launch
+// tag lives in Scratch::ctl[kCtlEpoch]; the work-queue counters of a launch are the 4 words at
+// ctl[kCtlQueue + (tag % 3) * 32].
+#pragma once
+
+#include <stdint.h>
+
+namespace cdk {
+namespace fused {
+
+constexpr int kCtlEpoch = 0;    // ctl word: launch tag of the last completed launch
+constexpr int kCtlQueue = 32;   // ctl words: 3 x 32 (launch tag % 3) work-queue counters
+constexpr int kYZeroWord = 1023;  // t_count word: "y zeroed" flag of the launch
+
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_add_u32(unsigned* p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// A 16-byte streaming load the compiler may not sink towards its use (volatile asm keeps it
+// ahead of griddepcontrol.wait, so its DRAM latency overlaps the previous grid's tail).
+__device__ __forceinline__ uint4 ldg_early_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long tagged(uint32_t tag, uint32_t payload) {
+    return (static_cast<unsigned long long>(tag) << 32) | payload;
+}
+
+// Spin until the word carries `tag`; return its payload.
+__device__ __forceinline__ uint32_t await_relaxed(const unsigned long long* p, uint32_t tag) {
+    unsigned long long w;
+    do {
+        w = ld_relaxed_u64(p);
+    } while (static_cast<uint32_t>(w >> 32) != tag);
+    return static_cast<uint32_t>(w);
+}
+
+__device__ __forceinline__ uint32_t await_acquire(const unsigned long long* p, uint32_t tag) {
+    unsigned long long w;
+    do {
+        w = ld_acquire_u64(p);
+    } while (static_cast<uint32_t>(w >> 32) != tag);
+    return static_cast<uint32_t>(w);
+}
+
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+
+}  // namespace fused
+}  // namespace cdk

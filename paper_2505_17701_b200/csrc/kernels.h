@@ -57,6 +57,7 @@ struct Scratch {
     unsigned* ctl = nullptr;                  // [0] launch tag of the last completed launch
     unsigned long long* t_lat = nullptr;      // kMaxBatchFast x 2048 : latent values
     unsigned long long* t_list = nullptr;     // F : rest-list entries (neuron id | bits << 27)
+    unsigned long long* t_aux = nullptr;      // F : per-entry payload (M-CountDown: u)
     unsigned long long* t_count = nullptr;    // kMaxCtas : rest-list length per CTA
     unsigned long long* t_alive = nullptr;    // kMaxCtas x kMaxBatchFast : alive counts per CTA
 };
@@ -98,6 +99,12 @@ cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, 
 cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
                             const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
                             int* alive_out, const LaunchCfg& c, int keep0 = 3);
+// M-CountDown step (batch 1) as one persistent kernel (kernels_fused_mc.cu): dense u = W_up x
+// over each CTA's neuron chunk, |u| > tau, compaction, and the sparse gate / down stage with
+// the work-stealing schedule.  Zeroes and accumulates y; optional mask / u / alive outputs.
+// Returns cudaErrorInvalidValue for shapes it does not cover (the caller uses the chain).
+cudaError_t launch_mc_fused(const LayerDev& L, const Scratch& S, const float* x, float tau, float* y,
+                            uint8_t* mask_out, float* u_out, int* alive_out, const LaunchCfg& c);
 // Host-supplied masks (exec_mc / exec_dc): ordered compaction + zero y (+ MC u gather).
 cudaError_t launch_compact_masks(const LayerDev& L, const Scratch& S, const uint8_t* masks,
                                  const float* u_full, int nb, float* y, const LaunchCfg& c);

@@ -1,1 +1,4 @@
-for k in 0 6 0 6; do CD_KEEP0=$k timeout 300 python bench.py --no-cpu-baseline --no-sweep 2>&1 | tail -1 | python -c "import json,sys; j=json.loads(sys.stdin.read()); print($k, j['ms_per_step']*1e3, j['roofline']['stages'][0]['us'])"; done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 600 python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "
+import json,sys; j=json.loads(sys.stdin.read()); print(j['ms_per_step']*1e3)
+for s in j['sweep']: print(s)"

@@ -96,6 +96,14 @@ CD_API int cd_layer_create_shard(int device, int64_t d_model, int64_t d_inter_to
 CD_API int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a,
                            const float* theta_b);
 
+/* read_model (model_io.cpp:140-224) straight to the device: parses and validates a CDWN1 model
+ * file exactly as the reference does (magic, header schema, byte counts, finite values ->
+ * CD_ERR_DATA with the reference's messages), uploads the layer in `dtype` and attaches a
+ * low-rank predictor.  dims_out[5] (optional) = {d_model, d_inter, d_rank, activation, seed};
+ * d_rank is 0 without a predictor and -1 for a ternary predictor (not attached: the B200 path
+ * runs the low-rank predictor only). */
+CD_API int cd_layer_load_cdwn1(int device, const char* path, int dtype, cd_layer** out, int64_t* dims_out);
+
 CD_API int cd_layer_destroy(cd_layer* h);
 
 CD_API int cd_layer_shape(const cd_layer* h, int64_t* d_model, int64_t* d_inter, int64_t* d_rank,

@@ -295,6 +295,8 @@ class Reference:
         L.ref_calibrate_mc.argtypes = [_i64, _i64, _f32p, _f32p, _i64, C.c_double, C.POINTER(C.c_double)]
         L.ref_traffic_split.argtypes = [C.c_int, _i64, _i64, _i64, _i64, _i64p]
         L.ref_flops.argtypes = [C.c_int, _i64, _i64, _i64, _i64, C.POINTER(_i64)]
+        L.ref_write_model.argtypes = [C.c_char_p, _u64, _i64, _i64, _i64, C.c_int, C.c_double]
+        L.ref_read_model.argtypes = [C.c_char_p, _i64p, vp, vp, vp, vp, vp]
 
     def _chk(self, rc: int):
         if rc != 0:
@@ -454,6 +456,24 @@ class Reference:
         out = _i64()
         self._chk(self.L.ref_flops(m, d, F, r, s, C.byref(out)))
         return int(out.value)
+
+
+    def write_model(self, path, seed, d, F, r=0, act=0, k=0.0):
+        """write_model (model_io.cpp:94-138) of the seeded bench() layer (+ predictor)."""
+        self._chk(self.L.ref_write_model(str(path).encode(), seed, d, F, r, act, k))
+
+    def read_model(self, path):
+        """read_model (model_io.cpp:140-224).  Raises ReferenceError_ (code 2 = DataError)."""
+        dims = np.zeros(5, np.int64)
+        self._chk(self.L.ref_read_model(str(path).encode(), dims, None, None, None, None, None))
+        d, F, r = int(dims[0]), int(dims[1]), int(dims[2])
+        up, gate, down = (np.empty((F, d), np.float32) for _ in range(3))
+        ta = np.empty((d, r), np.float32) if r > 0 else None
+        tb = np.empty((r, F), np.float32) if r > 0 else None
+        self._chk(self.L.ref_read_model(str(path).encode(), dims, _opt(up), _opt(gate), _opt(down), _opt(ta),
+                                        _opt(tb)))
+        return dict(d=d, F=F, r=r, act=int(dims[3]), seed=int(dims[4]), w_up=up, w_gate=gate, w_down=down,
+                    theta_a=ta, theta_b=tb)
 
 
 def reference_available() -> bool:

@@ -17,6 +17,7 @@
 #include "countdown/costmodel.hpp"
 #include "countdown/errors.hpp"
 #include "countdown/gated_mlp.hpp"
+#include "countdown/model_io.hpp"
 #include "countdown/predictor.hpp"
 #include "countdown/sparsity.hpp"
 
@@ -358,6 +359,47 @@ int ref_flops(int method, int64_t d, int64_t F, int64_t r, int64_t s_alive, int6
         s.d_rank = r;
         s.s_alive = s_alive;
         *out = method == 0 ? flops_dense(s) : method == 1 ? flops_cats(s) : method == 2 ? flops_mc(s) : flops_dc(s);
+    });
+}
+
+// write_model (model_io.cpp:94-138) of the seeded bench() workload: the layer of Rng(seed),
+// x discarded, a low-rank predictor of rank r from rng.fork() (r <= 0: no predictor).
+int ref_write_model(const char* path, uint64_t seed, int64_t d, int64_t F, int64_t r, int act, double k) {
+    return guarded([&] {
+        Rng rng(seed);
+        ModelFile mf;
+        mf.layer = make_random_layer(d, F, act == 0 ? Activation::Silu : Activation::GeluTanh, rng);
+        for (int64_t i = 0; i < d; ++i) (void)rng.normal_f();
+        mf.seed = seed;
+        if (r > 0) {
+            Rng prng = rng.fork();
+            mf.predictor = make_lowrank_predictor(d, r, F, prng);
+            mf.predictor_k = k;
+        }
+        write_model(path, mf);
+    });
+}
+
+// read_model (model_io.cpp:140-224): dims[5] = {d, F, r, act, seed}; any array may be NULL.
+int ref_read_model(const char* path, int64_t* dims, float* up, float* gate, float* down, float* ta,
+                   float* tb) {
+    return guarded([&] {
+        ModelFile mf = read_model(path);
+        dims[0] = mf.layer.d_model;
+        dims[1] = mf.layer.d_inter;
+        dims[2] = mf.predictor && mf.predictor->kind() == PredictorKind::LowRank ? mf.predictor->lowrank().d_rank : 0;
+        dims[3] = mf.layer.activation == Activation::Silu ? 0 : 1;
+        dims[4] = static_cast<int64_t>(mf.seed);
+        auto cp = [](const Mat32& m, float* out) {
+            if (out) std::memcpy(out, m.data.data(), m.data.size() * sizeof(float));
+        };
+        cp(mf.layer.w_up, up);
+        cp(mf.layer.w_gate, gate);
+        cp(mf.layer.w_down, down);
+        if (dims[2] > 0) {
+            cp(mf.predictor->lowrank().theta_a, ta);
+            cp(mf.predictor->lowrank().theta_b, tb);
+        }
     });
 }
 

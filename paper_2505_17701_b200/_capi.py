@@ -48,6 +48,7 @@ _SIGNATURES = {
     "cd_layer_create": [_i32, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp],
     "cd_layer_create_shard": [_i32, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _vp],
     "cd_layer_set_predictor": [_vp, _i64, _vp, _vp],
+    "cd_layer_load_cdwn1": [_i32, C.c_char_p, _i32, _vp, _vp],
     "cd_layer_destroy": [_vp],
     "cd_layer_shape": [_vp, _vp, _vp, _vp, _vp, _vp],
     "cd_layer_device_bytes": [_vp, _vp],

@@ -39,7 +39,7 @@ __all__ = [
     "BenchStats", "DeviceLayer", "exec_dense", "exec_mc", "exec_cats", "exec_dc", "pipeline_dense",
     "pipeline_mc", "pipeline_cats", "pipeline_dc", "forward_sparse", "forward_practical", "predict_logits",
     "predict_mask", "calibrate", "realized_sparsity", "bench", "synth_workload", "synth_normals",
-    "DataError", "NumericError", "CudaError",
+    "DataError", "NumericError", "CudaError", "ModelFile", "read_model", "write_model", "checksum_hex",
 ]
 
 
@@ -234,6 +234,20 @@ class DeviceLayer:
                                               ptr(w_down), C.byref(out)))
             F = re_ - rb
         return DeviceLayer(out, d, F)
+
+    @staticmethod
+    def load(path: str, device_dtype: str = "bf16", device: int = 0) -> "DeviceLayer":
+        """cd_layer_load_cdwn1: a CDWN1 model file (model_io.cpp:94-224) parsed, validated and
+        uploaded by the library (no host copy of the weights is kept)."""
+        out = C.c_void_p()
+        dims = np.zeros(5, np.int64)
+        check(lib().cd_layer_load_cdwn1(device, str(path).encode(), _DTYPES[device_dtype], C.byref(out),
+                                        ptr(dims)))
+        dl = DeviceLayer(out, int(dims[0]), int(dims[1]), max(0, int(dims[2])))
+        dl.activation = Activation(int(dims[3]))
+        dl.seed = int(dims[4])
+        dl.predictor_kind = "lowrank" if dims[2] > 0 else ("ternary" if dims[2] < 0 else None)
+        return dl
 
     @staticmethod
     def predictor_only(p: LowRankPredictor, device_dtype: str = "f32", device: int = 0) -> "DeviceLayer":
@@ -683,6 +697,122 @@ def realized_sparsity(mask: ActivationMask) -> float:
     if mask.size() == 0:
         raise DataError("realized_sparsity: empty mask")
     return 1.0 - mask.alive_count / mask.size()
+
+
+# ---------------------------------------------------------------- model files (host side)
+@dataclass
+class ModelFile:
+    """model_io.hpp ModelFile: the layer, seed provenance, optional predictor and its k."""
+    layer: GatedMlpLayer
+    seed: int = 0
+    predictor: Predictor | None = None
+    predictor_k: float = 0.0
+
+
+_MAGIC = b"CDWN1"
+
+
+def checksum_hex(a) -> str:
+    """checksum_hex (model_io.cpp:82-92): FNV-1a 64 over the raw bytes, 16 hex digits."""
+    h = 14695981039346656037
+    for b in np.ascontiguousarray(a).tobytes():
+        h ^= b
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
+def write_model(path: str, mf: ModelFile) -> None:
+    """write_model (model_io.cpp:94-138): magic, u32 header length, compact JSON header with
+    sorted keys (nlohmann's dump order), f32 blobs W_up, W_gate, W_down, theta_a, theta_b."""
+    import json
+    mf.layer.validate()
+    pred = None
+    if mf.predictor is not None:
+        lp = mf.predictor.lowrank()
+        pred = {"d_rank": lp.d_rank, "k": mf.predictor_k, "kind": "lowrank"}
+    header = {"activation": "silu" if mf.layer.activation == Activation.Silu else "gelu",
+              "d_inter": mf.layer.d_inter, "d_model": mf.layer.d_model, "predictor": pred,
+              "schema": "v1", "seed": int(mf.seed)}
+    hs = json.dumps(header, separators=(",", ":"), sort_keys=True).encode()
+    with open(path, "wb") as f:
+        f.write(_MAGIC)
+        f.write(np.uint32(len(hs)).tobytes())
+        f.write(hs)
+        for m in (mf.layer.w_up, mf.layer.w_gate, mf.layer.w_down):
+            f.write(np.ascontiguousarray(m, np.float32).tobytes())
+        if mf.predictor is not None:
+            f.write(np.ascontiguousarray(lp.theta_a, np.float32).tobytes())
+            f.write(np.ascontiguousarray(lp.theta_b, np.float32).tobytes())
+
+
+def read_model(path: str, device_dtype: str = "f32", device: int = 0) -> ModelFile:
+    """read_model (model_io.cpp:140-224) on the host: same validation and error messages
+    (DataError); the returned layer uploads to the device on first use."""
+    import json
+    try:
+        buf = open(path, "rb").read()
+    except OSError:
+        raise DataError(f"cannot open '{path}' for reading")
+    if len(buf) < 5 or buf[:5] != _MAGIC:
+        raise DataError(f"{path}: not a model file (bad magic, expected CDWN1)")
+    if len(buf) < 9:
+        raise DataError(f"{path}: truncated header length")
+    hlen = int(np.frombuffer(buf[5:9], np.uint32)[0])
+    if len(buf) < 9 + hlen:
+        raise DataError(f"{path}: truncated header")
+    try:
+        h = json.loads(buf[9:9 + hlen])
+    except ValueError as e:
+        raise DataError(f"{path}: bad header JSON: {e}")
+    try:
+        if h["schema"] != "v1":
+            raise DataError(f"{path}: unsupported schema")
+        d, F, seed = int(h["d_model"]), int(h["d_inter"]), int(h["seed"])
+        act_name = h["activation"]
+    except (KeyError, TypeError) as e:
+        raise DataError(f"{path}: bad header field: {e}")
+    if act_name not in ("silu", "gelu"):
+        raise DataError(f"unknown activation '{act_name}' (expected silu|gelu)")
+    if d <= 0 or F <= 0:
+        raise DataError(f"{path}: non-positive dimensions in header")
+    mat = d * F * 4
+    expected = 3 * mat
+    pd = h.get("predictor")
+    r = 0
+    if pd is not None:
+        kind = pd.get("kind")
+        if kind == "lowrank":
+            r = int(pd["d_rank"])
+            if r <= 0:
+                raise DataError(f"{path}: non-positive predictor rank")
+            expected += (d * r + r * F) * 4
+        elif kind == "ternary":
+            raise DataError(f"{path}: ternary predictor: the B200 path runs the low-rank predictor only")
+        else:
+            raise DataError(f"{path}: unknown predictor kind '{kind}'")
+    payload = len(buf) - 9 - hlen
+    if payload != expected:
+        raise DataError(f"{path}: payload is {payload} bytes, expected {expected}")
+    blob = np.frombuffer(buf, np.float32, count=expected // 4, offset=9 + hlen)
+    names = ["w_up", "w_gate", "w_down"]
+    mats = [blob[i * d * F:(i + 1) * d * F].reshape(F, d) for i in range(3)]
+    for m, n in zip(mats, names):
+        bad = np.flatnonzero(~np.isfinite(m))
+        if bad.size:
+            raise DataError(f"{path}: {n} contains a non-finite value at index {bad[0]}")
+    act = Activation.Silu if act_name == "silu" else Activation.GeluTanh
+    layer = GatedMlpLayer(d, F, act, mats[0].copy(), mats[1].copy(), mats[2].copy(), device_dtype, device)
+    mf = ModelFile(layer, seed)
+    if r > 0:
+        ta = blob[3 * d * F:3 * d * F + d * r].reshape(d, r).copy()
+        tb = blob[3 * d * F + d * r:].reshape(r, F).copy()
+        for m, n in ((ta, "theta_a"), (tb, "theta_b")):
+            bad = np.flatnonzero(~np.isfinite(m))
+            if bad.size:
+                raise DataError(f"{path}: {n} contains a non-finite value at index {bad[0]}")
+        mf.predictor = Predictor(LowRankPredictor(d, r, F, ta, tb), device_dtype, device)
+        mf.predictor_k = float(pd["k"])
+    return mf
 
 
 # ---------------------------------------------------------------- synthetic workloads

@@ -7,6 +7,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <fstream>
+#include <map>
+#include <sstream>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -337,6 +341,91 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
     h->last_launches = launches;
 }
 
+// ---------------------------------------------------------------- CDWN1 model files
+// The reference's on-disk model container (model_io.cpp:94-224): magic "CDWN1", u32 header
+// length, JSON header, then little-endian f32 blobs W_up, W_gate, W_down and the optional
+// predictor.  A small JSON reader covers the header schema (objects, strings, numbers, null).
+struct JVal {
+    enum Kind { kNull, kNum, kStr, kObj } kind = kNull;
+    double num = 0.0;
+    std::string str;
+    std::map<std::string, JVal> obj;
+};
+
+struct JParser {
+    const std::string& s;
+    size_t i = 0;
+    void ws() {
+        while (i < s.size() && (s[i] == ' ' || s[i] == '\n' || s[i] == '\t' || s[i] == '\r')) ++i;
+    }
+    [[noreturn]] void bad() { throw std::runtime_error("bad header JSON"); }
+    std::string str() {
+        if (s[i] != '"') bad();
+        std::string out;
+        for (++i; i < s.size() && s[i] != '"'; ++i) {
+            if (s[i] == '\\') {
+                if (++i >= s.size()) bad();
+            }
+            out.push_back(s[i]);
+        }
+        if (i >= s.size()) bad();
+        ++i;
+        return out;
+    }
+    JVal value() {
+        ws();
+        if (i >= s.size()) bad();
+        JVal v;
+        if (s[i] == '{') {
+            v.kind = JVal::kObj;
+            ++i;
+            ws();
+            if (s[i] == '}') { ++i; return v; }
+            for (;;) {
+                ws();
+                std::string k = str();
+                ws();
+                if (s[i++] != ':') bad();
+                v.obj[k] = value();
+                ws();
+                if (s[i] == ',') { ++i; continue; }
+                if (s[i] == '}') { ++i; return v; }
+                bad();
+            }
+        }
+        if (s[i] == '"') {
+            v.kind = JVal::kStr;
+            v.str = str();
+            return v;
+        }
+        if (s.compare(i, 4, "null") == 0) {
+            i += 4;
+            return v;
+        }
+        size_t end = i;
+        while (end < s.size() && std::strchr("+-.0123456789eE", s[end])) ++end;
+        if (end == i) bad();
+        v.kind = JVal::kNum;
+        v.num = std::stod(s.substr(i, end - i));
+        i = end;
+        return v;
+    }
+};
+
+const JVal& jfield(const JVal& o, const char* k, const std::string& path) {
+    auto it = o.obj.find(k);
+    if (o.kind != JVal::kObj || it == o.obj.end())
+        fail(CD_ERR_DATA, path + ": bad header field: missing '" + k + "'");
+    return it->second;
+}
+
+void check_finite_blob(const float* p, size_t n, const std::string& path, const char* what) {
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(p[i]))
+            fail(CD_ERR_DATA, path + ": " + std::string(what) + " contains a non-finite value at index " +
+                                  std::to_string(i));
+}
+
 cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_t re, int act,
                       int dtype, const float* w_up, const float* w_gate, const float* w_down,
                       bool predictor_only = false) {
@@ -459,6 +548,93 @@ int cd_layer_create_shard(int device, int64_t d_model, int64_t d_inter_total, in
         if (!out) fail(CD_ERR_DATA, "out is null");
         *out = create_impl(device, d_model, d_inter_total, row_begin, row_end, activation, dtype, w_up,
                            w_gate, w_down);
+    });
+}
+
+int cd_layer_load_cdwn1(int device, const char* path, int dtype, cd_layer** out, int64_t* dims_out) {
+    return guarded([&] {
+        if (!out || !path) fail(CD_ERR_DATA, "load: null argument");
+        const std::string p(path);
+        std::ifstream in(p, std::ios::binary);
+        if (!in) fail(CD_ERR_DATA, "cannot open '" + p + "' for reading");
+        std::ostringstream oss;
+        oss << in.rdbuf();
+        const std::string buf = oss.str();
+        if (buf.size() < 5 || buf.compare(0, 5, "CDWN1") != 0)
+            fail(CD_ERR_DATA, p + ": not a model file (bad magic, expected CDWN1)");
+        if (buf.size() < 9) fail(CD_ERR_DATA, p + ": truncated header length");
+        uint32_t hlen = 0;
+        std::memcpy(&hlen, buf.data() + 5, 4);
+        if (buf.size() < 9 + static_cast<size_t>(hlen)) fail(CD_ERR_DATA, p + ": truncated header");
+        const std::string hs = buf.substr(9, hlen);
+        JVal h;
+        try {
+            JParser jp{hs};
+            h = jp.value();
+        } catch (const std::exception& e) {
+            fail(CD_ERR_DATA, p + ": bad header JSON: " + e.what());
+        }
+        const JVal& schema = jfield(h, "schema", p);
+        if (schema.kind != JVal::kStr || schema.str != "v1") fail(CD_ERR_DATA, p + ": unsupported schema");
+        const int64_t d = static_cast<int64_t>(jfield(h, "d_model", p).num);
+        const int64_t F = static_cast<int64_t>(jfield(h, "d_inter", p).num);
+        const std::string act_name = jfield(h, "activation", p).str;
+        int act = -1;
+        if (act_name == "silu") act = CD_ACT_SILU;
+        else if (act_name == "gelu") act = CD_ACT_GELU_TANH;
+        else fail(CD_ERR_DATA, "unknown activation '" + act_name + "' (expected silu|gelu)");
+        const double seed = jfield(h, "seed", p).num;
+        if (d <= 0 || F <= 0) fail(CD_ERR_DATA, p + ": non-positive dimensions in header");
+        const size_t mat = static_cast<size_t>(d) * static_cast<size_t>(F);
+        size_t expected = 3 * mat * 4;
+        int64_t r = 0;  // 0: no predictor, -1: ternary (not attached: no B200 path)
+        auto pit = h.obj.find("predictor");
+        if (pit != h.obj.end() && pit->second.kind == JVal::kObj) {
+            const std::string kind = jfield(pit->second, "kind", p).str;
+            (void)jfield(pit->second, "k", p);
+            if (kind == "lowrank") {
+                r = static_cast<int64_t>(jfield(pit->second, "d_rank", p).num);
+                if (r <= 0) fail(CD_ERR_DATA, p + ": non-positive predictor rank");
+                expected += (static_cast<size_t>(d) * r + static_cast<size_t>(r) * F) * 4;
+            } else if (kind == "ternary") {
+                r = -1;
+                expected += 4 + mat * 4;
+            } else {
+                fail(CD_ERR_DATA, p + ": unknown predictor kind '" + kind + "'");
+            }
+        }
+        const size_t payload = buf.size() - 9 - hlen;
+        if (payload != expected)
+            fail(CD_ERR_DATA, p + ": payload is " + std::to_string(payload) + " bytes, expected " +
+                                  std::to_string(expected));
+        const float* blob = reinterpret_cast<const float*>(buf.data() + 9 + hlen);
+        if ((reinterpret_cast<uintptr_t>(blob) & 3) != 0) {
+            // unaligned header length: copy the payload to an aligned buffer
+            static thread_local std::vector<float> aligned;
+            aligned.resize(payload / 4);
+            std::memcpy(aligned.data(), blob, payload);
+            blob = aligned.data();
+        }
+        check_finite_blob(blob, mat, p, "w_up");
+        check_finite_blob(blob + mat, mat, p, "w_gate");
+        check_finite_blob(blob + 2 * mat, mat, p, "w_down");
+        std::unique_ptr<cd_layer> hl(create_impl(device, d, F, 0, F, act, dtype, blob, blob + mat, blob + 2 * mat));
+        if (r > 0) {
+            const float* ta = blob + 3 * mat;
+            const float* tb = ta + d * r;
+            check_finite_blob(ta, static_cast<size_t>(d * r), p, "theta_a");
+            check_finite_blob(tb, static_cast<size_t>(r * F), p, "theta_b");
+            const int rc = cd_layer_set_predictor(hl.get(), r, ta, tb);
+            if (rc != CD_OK) throw Fail{rc};
+        }
+        if (dims_out) {
+            dims_out[0] = d;
+            dims_out[1] = F;
+            dims_out[2] = r;
+            dims_out[3] = act;
+            dims_out[4] = static_cast<int64_t>(seed);
+        }
+        *out = hl.release();
     });
 }
 

@@ -399,3 +399,23 @@ def test_cats_pipeline(oracle, shape, act, dtype):
     check_mask_flips(fast.mask.alive, want_mask, tr["h"], tau, 1e-4)
     assert rel_l2(fast.y, oracle.forward_sparse(g, x, fast.mask.alive, act=act)) <= 1e-4
     assert rel_l2(cd.exec_cats(layer, x, tr["h"], want_mask, FAST), want) <= 1e-4
+
+
+# ----------------------------------------------------------------------------- calibration
+def test_gpu_calibration_matches_reference(oracle, reference):
+    """calibrate (calibration.cpp:11-37) for M-CountDown: tau_hat = mean over samples of each
+    sample's exact top-m |u| threshold -- bitwise the reference's (u from the exact kernels)."""
+    g = oracle.generate(77, 64, 256, 16)
+    layer = cd.GatedMlpLayer(64, 256, 0, g["w_up"], g["w_gate"], g["w_down"])
+    xs = np.stack([oracle.rng(500 + i).normals_f(64) for i in range(9)])
+    for k in (0.5, 0.7, 0.9):
+        got = cd.calibrate(layer, xs, k, cd.SparsityMethod.MCountdown)
+        want = reference.calibrate_mc(g["w_up"], xs, k)
+        assert got == want
+    # D-CountDown: the same rule on the predictor logits (signed)
+    pred = cd.Predictor(cd.LowRankPredictor(64, 16, 256, g["theta_a"], g["theta_b"]))
+    tau = cd.calibrate(layer, xs, 0.8, cd.SparsityMethod.DCountdown, pred)
+    zs = [oracle.lowrank_logits(g["theta_a"], g["theta_b"], x)[1] for x in xs]
+    m = cd.alive_count_for(0.8, 256)
+    want = np.mean([float(np.sort(z)[::-1][m]) for z in zs])
+    assert abs(tau - want) <= 1e-6 * max(1.0, abs(want))

@@ -115,6 +115,14 @@ CD_API int cd_layer_device_bytes(const cd_layer* h, int64_t* bytes);
 /* Kernel launches issued by the most recent forward call on this handle. */
 CD_API int cd_layer_last_launches(const cd_layer* h, int* launches);
 
+/* Engine that ran the most recent forward call: CD_PATH_EXACT (ordered folds, CUDA cores),
+ * CD_PATH_FAST (fused sparse kernels, CUDA cores, batch chunks of 4) or CD_PATH_TENSOR
+ * (bf16 layer at batch >= 8: masked row-union GEMM on the tcgen05 tensor cores). */
+#define CD_PATH_EXACT 0
+#define CD_PATH_FAST 1
+#define CD_PATH_TENSOR 2
+CD_API int cd_layer_last_path(const cd_layer* h, int* path);
+
 /* ---------------------------------------------------------------- host-buffer operators
  * Synchronous: inputs are read from host memory, outputs written to host memory before
  * return.  Optional outputs may be NULL. */

@@ -53,6 +53,7 @@ _SIGNATURES = {
     "cd_layer_shape": [_vp, _vp, _vp, _vp, _vp, _vp],
     "cd_layer_device_bytes": [_vp, _vp],
     "cd_layer_last_launches": [_vp, _vp],
+    "cd_layer_last_path": [_vp, _vp],
     "cd_exec_dense": [_vp, _i64, _vp, _i32, _vp],
     "cd_exec_mc": [_vp, _i64, _vp, _vp, _vp, _i32, _vp],
     "cd_exec_dc": [_vp, _i64, _vp, _vp, _i32, _vp],

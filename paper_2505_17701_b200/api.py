@@ -283,6 +283,12 @@ class DeviceLayer:
         check(lib().cd_layer_last_launches(self.raw, C.byref(v)))
         return int(v.value)
 
+    def last_path(self) -> str:
+        """Engine of the most recent forward call: "exact", "fast" or "tensor"."""
+        v = C.c_int()
+        check(lib().cd_layer_last_path(self.raw, C.byref(v)))
+        return ("exact", "fast", "tensor")[v.value]
+
     # ---- host-buffer operators (batch-first arrays)
     def exec_dense(self, x, reduction) -> np.ndarray:
         x = _f32(x)

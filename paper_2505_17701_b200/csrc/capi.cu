@@ -21,6 +21,7 @@
 
 #include "../../include/countdown_b200.h"
 #include "kernels.h"
+#include "kernels_tc.h"
 
 namespace {
 
@@ -53,6 +54,33 @@ template <typename F> int guarded(F&& f) {
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// A device (or pinned host) buffer that only grows; freed with its owner.
+struct Grow {
+    bool host = false;
+    void* p = nullptr;
+    size_t cap = 0;
+    Grow() = default;
+    explicit Grow(bool on_host) : host(on_host) {}
+    Grow(const Grow&) = delete;
+    Grow& operator=(const Grow&) = delete;
+    template <typename T> T* get(size_t n) {
+        const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+        if (bytes > cap) {
+            release();
+            const size_t want = std::max(bytes, cap * 2);
+            ck(host ? cudaMallocHost(&p, want) : cudaMalloc(&p, want), host ? "cudaMallocHost" : "cudaMalloc");
+            cap = want;
+        }
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) host ? cudaFreeHost(p) : cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    ~Grow() { release(); }
+};
+
 }  // namespace
 
 struct cd_layer {
@@ -67,7 +95,14 @@ struct cd_layer {
     std::vector<void*> host_allocs;
     int64_t bytes = 0;
     int last_launches = 0;
+    int last_path = CD_PATH_FAST;
     bool use_fused = true;  // D-CountDown as one persistent kernel (CD_DC_CHAIN=1 forces the chain)
+    bool use_tc = true;     // batches >= kTcMinBatch of a bf16 layer on the tensor cores (CD_TC=0: off)
+    cublasHandle_t blas = nullptr;
+    Grow tc_ws, blas_ws;    // tensor-core path workspace; cuBLAS workspace (graph-capture safe)
+    // large-batch staging (host-buffer calls on the tensor-core path)
+    Grow g_dx, g_dy, g_dmask_in, g_dmask_out, g_du_in, g_dind, g_dalive;
+    Grow g_hx{true}, g_hy{true}, g_hmask{true}, g_hind{true}, g_halive{true};
     int keep0 = 0;          // fused kernel: own active neurons streamed before rebalancing (CD_KEEP0)
     // device staging for the host-buffer entry points
     float* d_x = nullptr;
@@ -104,6 +139,7 @@ struct cd_layer {
             cudaStreamSynchronize(stream);
             cudaStreamDestroy(stream);
         }
+        if (blas) cublasDestroy(blas);
         for (void* p : dev_allocs) cudaFree(p);
         for (void* p : host_allocs) cudaFreeHost(p);
     }
@@ -143,6 +179,28 @@ struct Req {
     cudaEvent_t* marks = nullptr;
 };
 
+constexpr int kTcMinBatch = 8;  // batches from here on run on the tensor cores (bf16 layers)
+
+// The tensor-core path (kernels_tc.cu) covers bf16 layers at batch >= 8: pipelines, dense, and
+// exec_dc (its masks act as the override); exec_mc / exec_cats with caller-given u stay on the
+// CUDA-core chain.
+bool tc_eligible(const cd_layer* h, const Req& r) {
+    if (!h->use_tc || h->L.dtype != CD_DTYPE_BF16 || !h->L.w_up || r.nb < kTcMinBatch || r.marks) return false;
+    if (r.reduction != CD_REDUCTION_UNORDERED) return false;
+    if (r.with_masks) return r.method == cdk::kDC;
+    return r.method != cdk::kDC || r.ovr || h->L.theta_bt;
+}
+
+cublasHandle_t blas_of(cd_layer* h) {
+    if (!h->blas) {
+        if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) fail(CD_ERR_CUDA, "cublasCreate failed");
+        const size_t ws = 32u << 20;
+        if (cublasSetWorkspace(h->blas, h->blas_ws.get<uint8_t>(ws), ws) != CUBLAS_STATUS_SUCCESS)
+            fail(CD_ERR_CUDA, "cublasSetWorkspace failed");
+    }
+    return h->blas;
+}
+
 // Enqueue one operator call (device pointers) on r.stream.  Returns the number of launches.
 int run_chain(cd_layer* h, const Req& r) {
     const cdk::LayerDev& L = h->L;
@@ -165,6 +223,18 @@ int run_chain(cd_layer* h, const Req& r) {
         fail(CD_ERR_DATA, "pipeline_dc: layer has no low-rank predictor attached");
     if (!L.w_up) fail(CD_ERR_DATA, "forward: handle holds only a predictor (no layer weights)");
 
+    if (tc_eligible(h, r)) {
+        const cdk::tc::Plan p = cdk::tc::plan_for(r.nb, r.method);
+        void* ws = h->tc_ws.get<uint8_t>(cdk::tc::workspace_bytes(L, p, c.num_sms));
+        const uint8_t* ovr = r.with_masks ? r.masks_in : r.ovr;
+        ck(cdk::tc::launch_batched(L, p, ws, S.tc_flags, blas_of(h), r.method, r.nb, r.x, r.tau, ovr, r.y, r.mask_out,
+                                   r.ind_out, r.alive_out, c),
+           "batched (tensor cores)");
+        h->last_path = CD_PATH_TENSOR;
+        // own kernels: x pack, [latent fold], gate/up, down (+ the cuBLAS latent GEMM for DC)
+        return 3 + (r.method == cdk::kDC && !ovr ? 1 : 0);
+    }
+    h->last_path = r.reduction == CD_REDUCTION_UNORDERED ? CD_PATH_FAST : CD_PATH_EXACT;
     if (r.reduction == CD_REDUCTION_UNORDERED) {
         for (int c0 = 0; c0 < r.nb; c0 += kMaxBatchFast) {
             const int n = std::min(kMaxBatchFast, r.nb - c0);
@@ -299,44 +369,62 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
     const int64_t d = h->L.d, F = h->L.F;
     cudaStream_t s = h->stream;
     int launches = 0;
-    for (int64_t c0 = 0; c0 < batch; c0 += kMaxBatch) {
-        const int n = static_cast<int>(std::min<int64_t>(kMaxBatch, batch - c0));
-        std::memcpy(h->h_x, io.x + c0 * d, sizeof(float) * n * d);
-        ck(cudaMemcpyAsync(h->d_x, h->h_x, sizeof(float) * n * d, cudaMemcpyHostToDevice, s), "H2D x");
+    // the tensor-core path takes the whole batch at once (large-batch staging grows on demand)
+    Req probe = base;
+    probe.nb = static_cast<int>(std::min<int64_t>(batch, 1 << 30));
+    const int64_t chunk = tc_eligible(h, probe) ? batch : kMaxBatch;
+    const bool big = chunk > kMaxBatch;
+    const size_t cf = static_cast<size_t>(chunk * F), cd = static_cast<size_t>(chunk * d);
+    float* d_x = big ? h->g_dx.get<float>(cd) : h->d_x;
+    float* d_y = big ? h->g_dy.get<float>(cd) : h->d_y;
+    int* d_alive = big ? h->g_dalive.get<int>(chunk) : h->d_alive;
+    float* h_x = big ? h->g_hx.get<float>(cd) : h->h_x;
+    float* h_y = big ? h->g_hy.get<float>(cd) : h->h_y;
+    int* h_alive = big ? h->g_halive.get<int>(chunk) : h->h_alive;
+    const bool need_mask = io.masks_in || io.ovr || io.mask_out;
+    uint8_t* d_mask_in = big ? ((io.masks_in || io.ovr) ? h->g_dmask_in.get<uint8_t>(cf) : nullptr) : h->d_mask_in;
+    uint8_t* d_mask_out = big ? (io.mask_out ? h->g_dmask_out.get<uint8_t>(cf) : nullptr) : h->d_mask_out;
+    uint8_t* h_mask = big ? (need_mask ? h->g_hmask.get<uint8_t>(cf) : nullptr) : h->h_mask;
+    float* d_u_in = big ? (io.u_in ? h->g_du_in.get<float>(cf) : nullptr) : h->d_u_in;
+    float* d_ind = big ? (io.ind_out ? h->g_dind.get<float>(cf) : nullptr) : h->d_ind;
+    float* h_ind = big ? ((io.ind_out || io.u_in) ? h->g_hind.get<float>(cf) : nullptr) : h->h_ind;
+    for (int64_t c0 = 0; c0 < batch; c0 += chunk) {
+        const int n = static_cast<int>(std::min<int64_t>(chunk, batch - c0));
+        std::memcpy(h_x, io.x + c0 * d, sizeof(float) * n * d);
+        ck(cudaMemcpyAsync(d_x, h_x, sizeof(float) * n * d, cudaMemcpyHostToDevice, s), "H2D x");
         const uint8_t* masks = io.masks_in ? io.masks_in : io.ovr;
         if (masks) {
-            std::memcpy(h->h_mask, masks + c0 * F, static_cast<size_t>(n * F));
-            ck(cudaMemcpyAsync(h->d_mask_in, h->h_mask, n * F, cudaMemcpyHostToDevice, s), "H2D mask");
+            std::memcpy(h_mask, masks + c0 * F, static_cast<size_t>(n * F));
+            ck(cudaMemcpyAsync(d_mask_in, h_mask, n * F, cudaMemcpyHostToDevice, s), "H2D mask");
         }
         if (io.u_in) {
-            std::memcpy(h->h_ind, io.u_in + c0 * F, sizeof(float) * n * F);
-            ck(cudaMemcpyAsync(h->d_u_in, h->h_ind, sizeof(float) * n * F, cudaMemcpyHostToDevice, s), "H2D u");
+            std::memcpy(h_ind, io.u_in + c0 * F, sizeof(float) * n * F);
+            ck(cudaMemcpyAsync(d_u_in, h_ind, sizeof(float) * n * F, cudaMemcpyHostToDevice, s), "H2D u");
         }
-        // pinned staging is reused below: make sure the uploads have consumed it
         Req r = base;
         r.nb = n;
-        r.x = h->d_x;
-        r.y = h->d_y;
-        r.masks_in = io.masks_in ? h->d_mask_in : nullptr;
-        r.ovr = io.ovr ? h->d_mask_in : nullptr;
-        r.u_in = io.u_in ? h->d_u_in : nullptr;
-        r.mask_out = io.mask_out ? h->d_mask_out : nullptr;
-        r.ind_out = io.ind_out ? h->d_ind : nullptr;
-        r.alive_out = h->d_alive;
+        r.x = d_x;
+        r.y = d_y;
+        r.masks_in = io.masks_in ? d_mask_in : nullptr;
+        r.ovr = io.ovr ? d_mask_in : nullptr;
+        r.u_in = io.u_in ? d_u_in : nullptr;
+        r.mask_out = io.mask_out ? d_mask_out : nullptr;
+        r.ind_out = io.ind_out ? d_ind : nullptr;
+        r.alive_out = d_alive;
         r.stream = s;
         launches += run_chain(h, r);
-        ck(cudaMemcpyAsync(h->h_y, h->d_y, sizeof(float) * n * d, cudaMemcpyDeviceToHost, s), "D2H y");
-        ck(cudaMemcpyAsync(h->h_alive, h->d_alive, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "D2H alive");
-        if (io.mask_out)
-            ck(cudaMemcpyAsync(h->h_mask, h->d_mask_out, n * F, cudaMemcpyDeviceToHost, s), "D2H mask");
+        ck(cudaMemcpyAsync(h_y, d_y, sizeof(float) * n * d, cudaMemcpyDeviceToHost, s), "D2H y");
+        ck(cudaMemcpyAsync(h_alive, d_alive, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "D2H alive");
+        // pinned staging is reused below: the stream sync orders the uploads before the reuse
+        if (io.mask_out) ck(cudaMemcpyAsync(h_mask, d_mask_out, n * F, cudaMemcpyDeviceToHost, s), "D2H mask");
         if (io.ind_out)
-            ck(cudaMemcpyAsync(h->h_ind, h->d_ind, sizeof(float) * n * F, cudaMemcpyDeviceToHost, s), "D2H ind");
+            ck(cudaMemcpyAsync(h_ind, d_ind, sizeof(float) * n * F, cudaMemcpyDeviceToHost, s), "D2H ind");
         ck(cudaStreamSynchronize(s), "forward");
-        std::memcpy(io.y + c0 * d, h->h_y, sizeof(float) * n * d);
-        if (io.mask_out) std::memcpy(io.mask_out + c0 * F, h->h_mask, static_cast<size_t>(n * F));
-        if (io.ind_out) std::memcpy(io.ind_out + c0 * F, h->h_ind, sizeof(float) * n * F);
+        std::memcpy(io.y + c0 * d, h_y, sizeof(float) * n * d);
+        if (io.mask_out) std::memcpy(io.mask_out + c0 * F, h_mask, static_cast<size_t>(n * F));
+        if (io.ind_out) std::memcpy(io.ind_out + c0 * F, h_ind, sizeof(float) * n * F);
         if (io.alive_out)
-            for (int b = 0; b < n; ++b) io.alive_out[c0 + b] = h->h_alive[b];
+            for (int b = 0; b < n; ++b) io.alive_out[c0 + b] = h_alive[b];
     }
     h->last_launches = launches;
 }
@@ -496,8 +584,10 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     S.t_aux = h->dalloc<unsigned long long>(L.F);
     S.t_count = h->dalloc<unsigned long long>(cdk::kMaxCtas);
     S.t_alive = h->dalloc<unsigned long long>(cdk::kMaxCtas * kMaxBatchFast);
+    S.tc_flags = h->dalloc<unsigned>(cdk::kMaxCtas);
     if (const char* env = std::getenv("CD_DC_CHAIN")) h->use_fused = env[0] != '1';
     if (const char* env = std::getenv("CD_KEEP0")) h->keep0 = std::atoi(env);
+    if (const char* env = std::getenv("CD_TC")) h->use_tc = env[0] != '0';
     S.ind = h->dalloc<float>(kMaxBatch * L.F);
     S.ex_s = h->dalloc<float>(kMaxBatch * L.F);
     h->d_x = h->dalloc<float>(kMaxBatch * d);
@@ -692,6 +782,14 @@ int cd_layer_shape(const cd_layer* h, int64_t* d_model, int64_t* d_inter, int64_
         if (d_rank) *d_rank = h->L.r;
         if (dtype) *dtype = h->L.dtype;
         if (activation) *activation = h->L.act;
+    });
+}
+
+int cd_layer_last_path(const cd_layer* h, int* path) {
+    return guarded([&] {
+        check_layer(h);
+        if (!path) fail(CD_ERR_DATA, "path is null");
+        *path = h->last_path;
     });
 }
 

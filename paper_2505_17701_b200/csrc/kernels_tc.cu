@@ -1,0 +1,894 @@
+// kernels_tc.cu -- batched decode (B >= 8) and dense prefill on the 5th-generation tensor cores.
+//
+// SURVEY.md section 8f row 1.  At batch 64 the union of the per-sample masks covers ~every
+// neuron (0.8^64 ~ 0), so the batched step streams ALL up/gate/down rows once and zeroes s per
+// sample -- a masked row-union GEMM.  The reference semantics stay per sample
+// (blocked_exec.cpp:252-298 for MC, :350-379 for DC; main.cpp:239-282 loops samples).
+//
+//   phase A (this file, k_tc_gateup): one CTA per 128-neuron tile x n-tile of samples.
+//       TMA (128B-swizzled boxes) -> smem ring -> tcgen05.mma (one elected thread) ->
+//       TMEM accumulators U = W_up X^T, G = W_gate X^T (+ Z = theta_b^T latent^T for D-CountDown)
+//       -> epilogue warps: tcgen05.ld, per-sample mask (z > tau | |u| > tau | |act(g)| > tau |
+//       override), s = u * act(g) or 0, written as bf16 (hi, lo) pairs; mask / indicator /
+//       alive-count outputs.
+//   phase B: y = S W_down, a plain GEMM (cuBLAS bf16 tensor-core GEMM, f32 out), then the
+//       hi + lo fold.  The D-CountDown latent x theta_a is a plain GEMM as well.
+//
+// Precision.  Decode ("split" mode) carries every activation operand as a pair of bf16 values
+// (hi = rn(v), lo = rn(v - hi)), so products with the bf16 weights are exact to ~2^-16 and the
+// f32 accumulation dominates: the result matches the CUDA-core path to ~1e-5 relative, and the
+// thresholds see the same logits.  Prefill (large token counts, dense) uses plain bf16
+// activations (standard bf16 inference numerics, 1e-2 bound).
+#include <cublas_v2.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "kernels_tc.h"
+#include "launch.cuh"
+
+namespace cdk {
+namespace tc {
+
+namespace {
+
+constexpr int kBM = 128;          // neurons per tile (UMMA M)
+constexpr int kBK = 64;           // K elements per stage: one 128-byte swizzle row of bf16
+constexpr int kEpiWarps = 8;      // two per TMEM lane group, each taking half of the samples
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 64 + kEpiThreads;  // warp 0 TMA, warp 1 MMA + TMEM owner, then the epilogue
+constexpr int kABytes = kBM * kBK * 2;  // 16 KB per A operand box
+
+// ---------------------------------------------------------------- tcgen05 / TMA primitives
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 bytes apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+// Instruction descriptor, kind::f16: bf16 x bf16 -> f32, both operands K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 8 consecutive f32 TMEM columns of this thread's lane.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+// 16 consecutive f32 TMEM columns of this thread's lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15},"
+        " [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---------------------------------------------------------------- phase A kernel
+//
+// Work: tiles = (128-neuron m-tile, n-tile of samples), tile-major with the n-tiles of one
+// m-tile adjacent (their weight boxes are shared through L2).  Each tile is nkb = kb_z + kb_x
+// k-blocks (the D-CountDown predictor blocks theta_b^T x latent first, then up/gate blocks).
+//
+// Stream-K schedule: the grid is one CTA per SM and CTA c owns the contiguous k-block range
+// [c U / G, (c+1) U / G) of all U = tiles x nkb k-blocks, so every SM streams the same number of
+// weight bytes (a tile-per-CTA grid leaves 40 of 148 SMs idle at the Qwen shape).  A range splits
+// into segments (one per tile it touches).  The segment holding a tile's k-block 0 (the LAST
+// segment of its CTA) finishes the tile: it adds the partial accumulators that the following
+// CTAs wrote for the rest of that tile -- their FIRST segments, so already available -- and runs
+// the epilogue.  Partials travel through an L2-resident workspace with one release flag per
+// CTA (the finisher resets it: self-cleaning across launches).  Needs all CTAs co-resident
+// (grid <= SMs, one CTA per SM).
+struct Seg {
+    int tile, kb0, kb1;
+};
+
+__device__ __forceinline__ int64_t range_lo(int c, int64_t U, int G) { return static_cast<int64_t>(c) * U / G; }
+
+// Segment `si` of CTA c's range; returns false past the end.
+__device__ __forceinline__ bool seg_at(int c, int si, int64_t U, int G, int nkb, Seg& sg) {
+    const int64_t u1 = range_lo(c + 1, U, G);
+    int64_t u = range_lo(c, U, G);
+    for (int i = 0;; ++i) {
+        if (u >= u1) return false;
+        const int t = static_cast<int>(u / nkb);
+        const int kb0 = static_cast<int>(u - static_cast<int64_t>(t) * nkb);
+        const int kb1 = static_cast<int>((kb0 + (u1 - u) < nkb ? kb0 + (u1 - u) : static_cast<int64_t>(nkb)));
+        if (i == si) {
+            sg = {t, kb0, kb1};
+            return true;
+        }
+        u += kb1 - kb0;
+    }
+}
+
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+constexpr int kOvr = 4;  // epilogue kind: D-CountDown with a given mask (override / exec_dc)
+
+template <int KIND, bool SPLIT, int ACT>
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUtensorMap m_gate,
+            const __grid_constant__ CUtensorMap m_x, const __grid_constant__ CUtensorMap m_tb,
+            const __grid_constant__ CUtensorMap m_lat, const GateUpArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int N = a.N;
+    const int stage_bytes = 2 * kABytes + N * kBK * 2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
+    uint64_t* empty = full + a.stages;
+    uint64_t* tfull = empty + a.stages;  // accumulators of a segment complete (MMA -> epilogue)
+    uint64_t* tempty = tfull + 1;        // accumulators drained (epilogue -> MMA)
+    uint64_t* pbar = tempty + 1;         // contributor partials landed in smem (finisher)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nkb = a.kb_z + a.kb_x;
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t U = static_cast<int64_t>(a.tiles) * nkb;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, kEpiThreads);
+        mbar_init(pbar, 1);
+        fence_mbar_init();
+        prefetch_map(&m_up);
+        prefetch_map(&m_gate);
+        prefetch_map(&m_x);
+        if (a.kb_z) {
+            prefetch_map(&m_tb);
+            prefetch_map(&m_lat);
+        }
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(a.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    auto stamp = [&](int k) {
+        if (a.tl) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.tl[c * 8 + k] = t;
+        }
+    };
+    if (threadIdx.x == 0) stamp(0);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- TMA producer: the CTA's k-blocks in order, one continuous ring
+            const uint64_t pw = policy_evict_first();  // weights: streamed once
+            const uint64_t px = policy_evict_last();   // activations: re-read by every neuron tile
+            int it = 0;
+            Seg sg;
+            for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+                const int m0 = (sg.tile / a.n_tiles) * kBM;
+                const int row0 = (sg.tile % a.n_tiles) * N;
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
+                    const int s = it % a.stages;
+                    if (it >= a.stages) mbar_wait(empty + s, ((it / a.stages) - 1) & 1);
+                    uint8_t* st = smem + s * stage_bytes;
+                    if (kb < a.kb_z) {
+                        mbar_arrive_expect_tx(full + s, kABytes + N * kBK * 2);
+                        tma_load_2d(st, &m_tb, kb * kBK, m0, full + s, pw);
+                        tma_load_2d(st + 2 * kABytes, &m_lat, kb * kBK, row0, full + s, px);
+                    } else {
+                        const int k = (kb - a.kb_z) * kBK;
+                        if (it == 0) stamp(1);
+                        mbar_arrive_expect_tx(full + s, 2 * kABytes + N * kBK * 2);
+                        tma_load_2d(st, &m_up, k, m0, full + s, pw);
+                        tma_load_2d(st + kABytes, &m_gate, k, m0, full + s, pw);
+                        tma_load_2d(st + 2 * kABytes, &m_x, k, row0, full + s, px);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---- MMA issuer: U at TMEM columns [0, N), G at [N, 2N), Z at [2N, 3N)
+            const uint32_t idesc = idesc_bf16(kBM, N);
+            const uint32_t tU = tmem, tG = tmem + N, tZ = tmem + 2 * N;
+            int it = 0;
+            Seg sg;
+            for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+                if (si > 0) {
+                    mbar_wait(tempty, (si - 1) & 1);  // the epilogue drained the previous segment
+                    tc_fence_after();
+                }
+                const int first_ug = max(sg.kb0, a.kb_z);
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
+                    const int s = it % a.stages;
+                    mbar_wait(full + s, (it / a.stages) & 1);
+                    tc_fence_after();
+                    const uint32_t base = smem_u32(smem + s * stage_bytes);
+                    const uint64_t da0 = sw128_desc(base), da1 = sw128_desc(base + kABytes),
+                                   db = sw128_desc(base + 2 * kABytes);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        // +32 bytes per 16-element K step inside the swizzle atom (descriptor units of 16 B)
+                        const uint64_t o = static_cast<uint64_t>(2 * k);
+                        if (kb < a.kb_z) {
+                            umma_bf16(tZ, da0 + o, db + o, idesc, (kb > sg.kb0 || k > 0) ? 1u : 0u);
+                        } else {
+                            const uint32_t acc = (kb > first_ug || k > 0) ? 1u : 0u;
+                            umma_bf16(tU, da0 + o, db + o, idesc, acc);
+                            umma_bf16(tG, da1 + o, db + o, idesc, acc);
+                        }
+                    }
+                    umma_commit(empty + s);  // frees the stage once these MMAs have read it
+                }
+                umma_commit(tfull);
+            }
+            stamp(2);
+        }
+    } else {
+        // ---- epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = the tile's neuron rows; the
+        // two warps of a lane group split the samples (columns) in halves
+        const int g = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int m = g * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0 .. kEpiThreads-1
+        const uint32_t trow = tmem + (static_cast<uint32_t>(g * 32) << 16);
+        constexpr bool kZ = KIND == kDC;
+        constexpr int kParts = kZ ? 3 : 2;
+        constexpr int kH = SPLIT ? 2 : 1;
+        constexpr int kC = 8;  // samples per chunk
+        Seg sg;
+        for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+            mbar_wait(tfull, si & 1);
+            tc_fence_after();
+            if (et == 0) stamp(3 + (si > 2 ? 2 : si));
+            const bool has_z = kZ && sg.kb0 < a.kb_z;
+            const bool has_ug = sg.kb1 > a.kb_z;
+            if (sg.kb0 > 0) {
+                // contributor: park the partial accumulators (hi + lo summed) in this CTA's
+                // workspace slot, laid out [part][sample][row]
+                float* slot = a.ws + static_cast<int64_t>(c) * kParts * a.nbt * kBM;
+                for (int q = 0; q < kParts; ++q) {
+                    if (q == 2 ? !has_z : !has_ug) continue;
+                    for (int c0 = half * 16; c0 < a.nbt; c0 += 32) {
+                        float v[16];
+                        tmem_ld16(trow + q * N + c0, v);
+                        if constexpr (SPLIT) {
+                            float w[16];
+                            tmem_ld16(trow + q * N + a.nbt + c0, w);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) v[j] += w[j];
+                        } else {
+                            tmem_wait_ld();
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) slot[(q * a.nbt + c0 + j) * kBM + m] = v[j];
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(tempty);
+                __threadfence();
+                named_bar_sync(1, kEpiThreads);
+                if (et == 0) st_release_u32(a.flags + c, 1u);
+                continue;
+            }
+            // finisher (holds k-block 0): gather the partials of the CTAs that follow
+            const int tile = sg.tile;
+            const int64_t tile_base = static_cast<int64_t>(tile) * nkb;
+            int c_last = c;
+            while (c_last + 1 < G && range_lo(c_last + 1, U, G) < tile_base + nkb) ++c_last;
+            // the contributors' partials, pulled into the (now idle) ring with bulk copies when
+            // they fit -- the finisher segment is its CTA's last, so no stage is in flight
+            const int64_t slot_floats = static_cast<int64_t>(kParts) * a.nbt * kBM;
+            const bool in_smem = (c_last - c) * slot_floats * 4 <= static_cast<int64_t>(a.stages) * stage_bytes;
+            if (c_last > c) {
+                if (et < c_last - c) {
+                    unsigned* f = a.flags + c + 1 + et;
+                    while (ld_acquire_u32(f) == 0u) {
+                    }
+                    *f = 0u;  // consumed: ready for the next launch
+                }
+                __threadfence();
+                named_bar_sync(1, kEpiThreads);
+                if (in_smem) {
+                    if (et == 0) {
+                        fence_proxy_async_smem();
+                        const uint32_t bytes = static_cast<uint32_t>(slot_floats * 4);
+                        mbar_arrive_expect_tx(pbar, bytes * (c_last - c));
+                        for (int cc = c + 1; cc <= c_last; ++cc)
+                            bulk_g2s(smem + (cc - c - 1) * bytes, a.ws + cc * slot_floats, bytes, pbar,
+                                     policy_evict_first());
+                    }
+                    mbar_wait(pbar, 0);
+                }
+            }
+            const int m0 = (tile / a.n_tiles) * kBM;
+            const int ntile = tile % a.n_tiles;
+            const int i = m0 + m;
+            const bool valid = i < a.F;
+            const int nbt = a.nbt;
+            const int64_t F = a.F;
+            const int64_t ld_s = a.ld_s;
+            const int64_t gb0 = static_cast<int64_t>(ntile) * nbt;
+            const int nlive = a.nb - gb0 < nbt ? static_cast<int>(a.nb - gb0) : nbt;
+            const int hb = nbt / 2;  // samples per half
+            const int sb0 = half * hb;
+            // this row's s outputs: sample sb of the tile -> hi row (pair layout) / token row
+            __nv_bfloat16* s_hi = a.s_out +
+                                  (SPLIT ? static_cast<int64_t>(ntile) * N : static_cast<int64_t>(ntile) * nbt) * ld_s +
+                                  static_cast<int64_t>(sb0) * ld_s + i;
+            const int64_t lo_step = static_cast<int64_t>(nbt) * ld_s;
+            for (int cb = sb0; cb < sb0 + hb; cb += kC, s_hi += kC * ld_s) {
+                float acc[kParts][kH][kC];
+#pragma unroll
+                for (int q = 0; q < kParts; ++q) {
+                    const bool own = q == 2 ? has_z : has_ug;
+#pragma unroll
+                    for (int h = 0; h < kH; ++h) {
+                        if (own) {
+                            tmem_ld8(trow + q * N + h * nbt + cb, acc[q][h]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < kC; ++j) acc[q][h][j] = 0.0f;
+                        }
+                    }
+                }
+                tmem_wait_ld();
+                if (c_last > c) {
+                    for (int cc = c + 1; cc <= c_last; ++cc) {
+                        const int64_t q0 = range_lo(cc, U, G) - tile_base;
+                        const int64_t q1 = range_lo(cc + 1, U, G) - tile_base;
+#pragma unroll
+                        for (int q = 0; q < kParts; ++q) {
+                            if (q == 2 ? !(q0 < a.kb_z) : !(q1 > a.kb_z)) continue;
+                            const int64_t off = (q * nbt + cb) * kBM + m;
+                            if (in_smem) {
+                                const float* sp = reinterpret_cast<const float*>(smem) + (cc - c - 1) * slot_floats + off;
+#pragma unroll
+                                for (int j = 0; j < kC; ++j) acc[q][0][j] += sp[j * kBM];
+                            } else {
+                                const float* gp = a.ws + cc * slot_floats + off;
+#pragma unroll
+                                for (int j = 0; j < kC; ++j) acc[q][0][j] += __ldcg(gp + j * kBM);
+                            }
+                        }
+                    }
+                }
+                unsigned on_bits = 0;
+                __nv_bfloat16* p = s_hi;
+#pragma unroll
+                for (int j = 0; j < kC; ++j, p += ld_s) {
+                    float u = acc[0][0][j], gg = acc[1][0][j], z = kZ ? acc[kParts - 1][0][j] : 0.0f;
+                    if constexpr (SPLIT) {
+                        u += acc[0][kH - 1][j];
+                        gg += acc[1][kH - 1][j];
+                        if constexpr (kZ) z += acc[kParts - 1][kH - 1][j];
+                    }
+                    const bool live = valid && cb + j < nlive;
+                    const float ag = act_fast(ACT, gg);
+                    bool on;
+                    if constexpr (KIND == kDC) {
+                        on = z > a.tau;
+                    } else if constexpr (KIND == kMC) {
+                        on = fabsf(u) > a.tau;
+                    } else if constexpr (KIND == kCATS) {
+                        on = fabsf(ag) > a.tau;
+                    } else if constexpr (KIND == kOvr) {
+                        on = live && a.ovr[(gb0 + cb + j) * F + i] != 0;
+                    } else {
+                        on = true;
+                    }
+                    on = on && live;
+                    on_bits |= on ? 1u << j : 0u;
+                    const float sv = on ? u * ag : 0.0f;
+                    if (live) {
+                        const __nv_bfloat16 hv = __float2bfloat16_rn(sv);
+                        *p = hv;
+                        if constexpr (SPLIT) p[lo_step] = __float2bfloat16_rn(sv - __bfloat162float(hv));
+                        if (a.ind_out) a.ind_out[(gb0 + cb + j) * F + i] = KIND == kDC ? z : KIND == kCATS ? ag : u;
+                    }
+                }
+                if (valid && a.mask_out) {
+                    for (int j = 0; j < kC && cb + j < nlive; ++j)
+                        a.mask_out[(gb0 + cb + j) * F + i] = (on_bits >> j) & 1u;
+                }
+                if (a.alive_out) {
+                    // per-sample counts: popc of the warp's ballot of each sample's bit
+#pragma unroll
+                    for (int j = 0; j < kC; ++j) {
+                        const unsigned bal = __ballot_sync(0xffffffffu, (on_bits >> j) & 1u);
+                        if (lane == j && bal) atomicAdd(a.alive_out + gb0 + cb + j, __popc(bal));
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty);
+        }
+        tc_fence_before();
+        if (et == 0) stamp(6);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) stamp(7);
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------- phase B kernel
+//
+// y (nb x d, f32, zeroed) += s W_down.  UMMA view: D[j][b] = sum_i W_down[i][j] s[b][i], so
+// A = W_down^T is MN-major (d is the contiguous dimension of each neuron's down row; TMA boxes of
+// 64 j x 64 i, 128B-swizzled), B = the s rows (K-major).  In split mode the hi and lo rows of s
+// are two MMAs into the SAME accumulator (D = W^T (s_hi + s_lo)^T), so no fold pass.  Tiles are
+// (128-column j-tile, n-tile), k-blocks 64 neurons; the same stream-K ranges as phase A, each
+// segment's partial reduced into y with red.global.add (TMEM double-buffered: segments do not
+// wait for each other's drain).
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr, uint32_t lbo_bytes) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(lbo_bytes >> 4) << 16) |
+           (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+constexpr int kDJ = 2;  // 128-column j sub-tiles per CTA tile (they share the s tile)
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_tc_down(const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_s, const DownArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int nbt = a.nbt;
+    const int brows = 2 * nbt;                    // B rows per stage: hi rows, then lo rows
+    constexpr int kABytesD = kDJ * kBM * kBK * 2;  // 2 x (two 64 x 64 boxes of W_down)
+    const int stage_bytes = kABytesD + brows * kBK * 2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
+    uint64_t* empty = full + a.stages;
+    uint64_t* tfull = empty + a.stages;  // [2]
+    uint64_t* tempty = tfull + 2;        // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nkb = a.kb;
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t U = static_cast<int64_t>(a.tiles) * nkb;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull + b, 1);
+            mbar_init(tempty + b, kEpiThreads);
+        }
+        fence_mbar_init();
+        prefetch_map(&m_w);
+        prefetch_map(&m_s);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(a.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pw = policy_evict_first();
+            const uint64_t ps = policy_evict_last();
+            int it = 0;
+            Seg sg;
+            for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+                const int j0 = (sg.tile / a.n_tiles) * kDJ * kBM;
+                const int row0 = (sg.tile % a.n_tiles) * brows;
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
+                    const int s = it % a.stages;
+                    if (it >= a.stages) mbar_wait(empty + s, ((it / a.stages) - 1) & 1);
+                    uint8_t* st = smem + s * stage_bytes;
+                    mbar_arrive_expect_tx(full + s, kABytesD + brows * kBK * 2);
+#pragma unroll
+                    for (int q = 0; q < 2 * kDJ; ++q)
+                        tma_load_2d(st + q * (kBK * kBK * 2), &m_w, j0 + 64 * q, kb * kBK, full + s, pw);
+                    tma_load_2d(st + kABytesD, &m_s, kb * kBK, row0, full + s, ps);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // D_q[j][b]: M = 128 j (A MN-major), N = nbt samples; q = j sub-tile
+            const uint32_t idesc = idesc_bf16(kBM, nbt) | (1u << 15);
+            int it = 0;
+            Seg sg;
+            for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+                const int buf = si & 1;
+                if (si >= 2) {
+                    mbar_wait(tempty + buf, ((si >> 1) - 1) & 1);
+                    tc_fence_after();
+                }
+                const uint32_t td = tmem + buf * kDJ * nbt;
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
+                    const int s = it % a.stages;
+                    mbar_wait(full + s, (it / a.stages) & 1);
+                    tc_fence_after();
+                    const uint32_t base = smem_u32(smem + s * stage_bytes);
+                    const uint64_t dbh = sw128_desc(base + kABytesD);
+                    const uint64_t dbl = sw128_desc(base + kABytesD + nbt * kBK * 2);
+#pragma unroll
+                    for (int q = 0; q < kDJ; ++q) {
+                        const uint64_t da = sw128_mn_desc(base + q * kBM * kBK * 2, kBK * kBK * 2);
+#pragma unroll
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            // A: 16 K-rows of 128 B per step (+2048 B); B: +32 B inside the swizzle atom
+                            const uint64_t oa = static_cast<uint64_t>(128 * k), ob = static_cast<uint64_t>(2 * k);
+                            umma_bf16(td + q * nbt, da + oa, dbh + ob, idesc, (kb > sg.kb0 || k > 0) ? 1u : 0u);
+                            umma_bf16(td + q * nbt, da + oa, dbl + ob, idesc, 1u);
+                        }
+                    }
+                    umma_commit(empty + s);
+                }
+                umma_commit(tfull + buf);
+            }
+        }
+    } else {
+        // epilogue: row j of a sub-tile = TMEM lane; warp half q takes sub-tile q
+        const int g = warp & 3;
+        const int q = (warp - 2) >> 2;
+        const int m = g * 32 + lane;
+        const uint32_t trow = tmem + (static_cast<uint32_t>(g * 32) << 16);
+        Seg sg;
+        for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+            const int buf = si & 1;
+            mbar_wait(tfull + buf, (si >> 1) & 1);
+            tc_fence_after();
+            const int j = (sg.tile / a.n_tiles) * kDJ * kBM + q * kBM + m;
+            const int64_t gb0 = static_cast<int64_t>(sg.tile % a.n_tiles) * nbt;
+            for (int cb = 0; cb < nbt; cb += 8) {
+                float v[8];
+                tmem_ld8(trow + (buf * kDJ + q) * nbt + cb, v);
+                tmem_wait_ld();
+                if (j < a.d) {
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        const int64_t b = gb0 + cb + t;
+                        if (b < a.nb) red_add_f32(a.y + b * a.d + j, v[t]);
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty + buf);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------- small element-wise kernels
+__device__ __forceinline__ void split_store4(__nv_bfloat16* hi, __nv_bfloat16* lo, float4 v) {
+    const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
+    const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+    const __nv_bfloat162 l0 = __floats2bfloat162_rn(v.x - f0.x, v.y - f0.y);
+    const __nv_bfloat162 l1 = __floats2bfloat162_rn(v.z - f1.x, v.w - f1.y);
+    uint2 hv, lv;
+    hv.x = *reinterpret_cast<const uint32_t*>(&h0);
+    hv.y = *reinterpret_cast<const uint32_t*>(&h1);
+    lv.x = *reinterpret_cast<const uint32_t*>(&l0);
+    lv.y = *reinterpret_cast<const uint32_t*>(&l1);
+    *reinterpret_cast<uint2*>(hi) = hv;
+    if (lo) *reinterpret_cast<uint2*>(lo) = lv;
+}
+
+// x (nb x d f32) -> xb (B-operand rows, ld elements, bf16).  split: sample b of n-tile t goes to
+// rows t N + j (hi) and t N + nbt + j (lo), j = b % nbt.  Grid (ceil(d / 1024), nb), 256 threads,
+// 4 columns per thread (d % 4 == 0; scalar otherwise).
+__global__ void k_tc_pack_x(const float* __restrict__ x, int64_t d, int64_t ld, int split, int nbt,
+                            __nv_bfloat16* __restrict__ xb) {
+    const int64_t b = blockIdx.y;
+    const int64_t r = split ? (b / nbt) * 2 * nbt + b % nbt : b;
+    __nv_bfloat16* hi = xb + r * ld;
+    __nv_bfloat16* lo = split ? xb + (r + nbt) * ld : nullptr;
+    const float* xr = x + b * d;
+    const int64_t c = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if ((d & 3) == 0) {
+        if (c < d) split_store4(hi + c, lo ? lo + c : nullptr, *reinterpret_cast<const float4*>(xr + c));
+        return;
+    }
+    for (int64_t k = c; k < c + 4 && k < d; ++k) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(xr[k]);
+        hi[k] = h;
+        if (lo) lo[k] = __float2bfloat16_rn(xr[k] - __bfloat162float(h));
+    }
+}
+
+// Latent pairs from the f32 GEMM output: fold hi + lo rows, re-split into bf16 pairs.
+__global__ void k_tc_fold_split(const float* __restrict__ in, int64_t ldi, int64_t ncols, int nbt,
+                                __nv_bfloat16* __restrict__ outp, int64_t ldo) {
+    const int64_t b = blockIdx.y;
+    const int64_t r = (b / nbt) * 2 * nbt + b % nbt;
+    for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < ncols;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const float v = in[r * ldi + c] + in[(r + nbt) * ldi + c];
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        outp[r * ldo + c] = h;
+        outp[(r + nbt) * ldo + c] = __float2bfloat16_rn(v - __bfloat162float(h));
+    }
+}
+
+
+// ---------------------------------------------------------------- host: tensor maps, cuBLAS
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 map: `rows` rows of `cols` elements, `stride_elems` apart; boxes of 64 x box_rows,
+// 128-byte swizzle; out-of-range elements read as zero.
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t stride_elems, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride_elems * 2)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t cublas_status(cublasStatus_t s) { return s == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown; }
+
+// Row-major C (rows x n, ldc) = A (rows x k, lda) * W, W k x n row-major (ldw).
+cudaError_t gemm_rows_w(cublasHandle_t h, int64_t rows, int64_t n, int64_t k, const void* A, int64_t lda,
+                        const void* W, int64_t ldw, float* C, int64_t ldc) {
+    const float one = 1.0f, zero = 0.0f;
+    return cublas_status(cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows),
+                                      static_cast<int>(k), &one, W, CUDA_R_16BF, static_cast<int>(ldw), A,
+                                      CUDA_R_16BF, static_cast<int>(lda), &zero, C, CUDA_R_32F,
+                                      static_cast<int>(ldc), CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+}
+
+}  // namespace
+
+int64_t round_up64(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+Plan plan_for(int64_t nb, int method) {
+    Plan p;
+    // Decode: pairs of bf16 (hi, lo) per activation, up to 64 samples per n-tile (UMMA N = 128).
+    // Large dense batches (prefill): single bf16 activations, 256 tokens per n-tile.
+    p.split = !(method == kDense && nb > 256);
+    if (p.split) {
+        p.nbt = static_cast<int>(std::min<int64_t>(64, round_up64(nb, 16)));  // epilogue chunks of 16
+        p.N = 2 * p.nbt;
+    } else {
+        p.nbt = 256;
+        p.N = 256;
+    }
+    p.n_tiles = static_cast<int>((nb + p.nbt - 1) / p.nbt);
+    p.rows = static_cast<int64_t>(p.n_tiles) * p.N;
+    return p;
+}
+
+size_t workspace_bytes(const LayerDev& L, const Plan& p, int num_sms) {
+    const int64_t ldr = L.ldr > 0 ? L.ldr : 8;
+    size_t b = 0;
+    b += round_up64(p.rows * L.ld * 2, 256);              // xb
+    b += round_up64(p.rows * round_up64(L.F, 8) * 2, 256);  // s
+    b += round_up64(p.rows * ldr * 2, 256);               // latent (pairs)
+    b += round_up64(p.rows * ldr * 4, 256);               // latent f32 GEMM output
+    b += round_up64(static_cast<int64_t>(num_sms) * 3 * p.N * kBM * 4, 256);  // stream-K partials
+    return b;
+}
+
+cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned* flags, cublasHandle_t blas,
+                           int method, int64_t nb,
+                           const float* x, float tau, const uint8_t* ovr, float* y, uint8_t* mask_out,
+                           float* ind_out, int* alive_out, const LaunchCfg& c) {
+    if (L.dtype != 1 /* bf16 */ || !L.w_up) return cudaErrorInvalidValue;
+    if (method == kDC && !ovr && !L.theta_bt) return cudaErrorInvalidValue;
+    const int64_t ldr = L.ldr > 0 ? L.ldr : 8;
+    const int64_t ld_s = round_up64(L.F, 8);
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    auto take = [&](size_t bytes) {
+        uint8_t* q = w;
+        w += round_up64(static_cast<int64_t>(bytes), 256);
+        return q;
+    };
+    auto* xb = reinterpret_cast<__nv_bfloat16*>(take(p.rows * L.ld * 2));
+    auto* sb = reinterpret_cast<__nv_bfloat16*>(take(p.rows * ld_s * 2));
+    auto* latb = reinterpret_cast<__nv_bfloat16*>(take(p.rows * ldr * 2));
+    auto* lat32 = reinterpret_cast<float*>(take(p.rows * ldr * 4));
+    auto* ws_partial = reinterpret_cast<float*>(take(static_cast<size_t>(c.num_sms) * 3 * p.N * kBM * 4));
+    const bool dc_pred = method == kDC && !ovr;
+
+    cudaError_t e = cudaSuccess;
+    if (cublasSetStream(blas, c.stream) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    k_tc_pack_x<<<dim3(static_cast<unsigned>((L.d + 1023) / 1024), static_cast<unsigned>(nb)), 256, 0, c.stream>>>(
+        x, L.d, L.ld, p.split, p.nbt, xb);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (dc_pred) {
+        // latent pairs = x theta_a (theta_a is d x ldr row-major, the reference layout)
+        e = gemm_rows_w(blas, p.rows, L.r, L.d, xb, L.ld, L.theta_a, ldr, lat32, ldr);
+        if (e != cudaSuccess) return e;
+        k_tc_fold_split<<<dim3(static_cast<unsigned>((L.r + 255) / 256), static_cast<unsigned>(nb)), 256, 0,
+                          c.stream>>>(lat32, ldr, L.r, p.nbt, latb, ldr);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (alive_out && (e = cudaMemsetAsync(alive_out, 0, sizeof(int) * nb, c.stream)) != cudaSuccess) return e;
+
+    CUtensorMap m_up, m_gate, m_x, m_tb, m_lat;
+    bool ok = make_map(&m_up, L.w_up, L.F, L.d, L.rs, kBM) && make_map(&m_gate, L.w_gate, L.F, L.d, L.rs, kBM) &&
+              make_map(&m_x, xb, p.rows, L.d, L.ld, p.N);
+    if (dc_pred) {
+        ok = ok && make_map(&m_tb, L.theta_bt, L.F, L.r, ldr, kBM) && make_map(&m_lat, latb, p.rows, L.r, ldr, p.N);
+    } else {
+        m_tb = m_up;
+        m_lat = m_x;
+    }
+    if (!ok) return cudaErrorInvalidValue;
+
+    GateUpArgs a;
+    a.F = static_cast<int>(L.F);
+    a.nb = static_cast<int>(nb);
+    a.nbt = p.nbt;
+    a.N = p.N;
+    a.kb_x = static_cast<int>((L.d + kBK - 1) / kBK);
+    a.kb_z = dc_pred ? static_cast<int>((L.r + kBK - 1) / kBK) : 0;
+    a.tau = tau;
+    static const int st_env = [] {
+        const char* e = std::getenv("CD_TC_STAGES");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.ovr = ovr;
+    a.s_out = sb;
+    a.ld_s = ld_s;
+    a.mask_out = mask_out;
+    a.ind_out = ind_out;
+    a.alive_out = alive_out;
+    const int used_cols = (dc_pred ? 3 : 2) * p.N;
+    a.tmem_cols = used_cols <= 32 ? 32 : used_cols <= 64 ? 64 : used_cols <= 128 ? 128 : used_cols <= 256 ? 256 : 512;
+    if (used_cols > 512) return cudaErrorInvalidValue;
+    a.n_tiles = p.n_tiles;
+    a.tiles = static_cast<int>((L.F + kBM - 1) / kBM) * p.n_tiles;
+    const int64_t units = static_cast<int64_t>(a.tiles) * (a.kb_x + a.kb_z);
+    static const int grid_env = [] {
+        const char* e = std::getenv("CD_TC_GRID");
+        return e ? std::atoi(e) : 0;
+    }();
+    static unsigned long long* tl_env = [] {
+        const char* e = std::getenv("CD_TC_TL");  // development: device buffer for phase stamps
+        return e ? reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 10)) : nullptr;
+    }();
+    a.tl = tl_env;
+    int grid = static_cast<int>(std::min<int64_t>(std::min(c.num_sms, kMaxCtas), units));
+    if (grid_env > 0 && grid_env < grid) grid = grid_env;
+    a.ws = ws_partial;
+    a.flags = flags;
+    const int stage_bytes = 2 * kABytes + p.N * kBK * 2;
+    const size_t fixed = 1024 + 256;
+    a.stages = static_cast<int>(std::min<size_t>(8, (kMaxDynSmem - fixed) / stage_bytes));
+    if (st_env > 0) a.stages = std::min(a.stages, st_env);
+    const size_t smem = fixed + static_cast<size_t>(a.stages) * stage_bytes;
+    using KFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GateUpArgs);
+    const int kind = ovr ? kOvr : method;
+    KFn fn = nullptr;
+#define CD_TC_PICK(K, S)                                                                      \
+    if (kind == K && p.split == S) fn = L.act == 0 ? k_tc_gateup<K, S, 0> : k_tc_gateup<K, S, 1>;
+    CD_TC_PICK(kDense, true)
+    CD_TC_PICK(kDense, false)
+    CD_TC_PICK(kMC, true)
+    CD_TC_PICK(kDC, true)
+    CD_TC_PICK(kCATS, true)
+    CD_TC_PICK(kOvr, true)
+#undef CD_TC_PICK
+    if (!fn) return cudaErrorInvalidValue;
+    if ((e = set_smem(fn, smem)) != cudaSuccess) return e;
+    fn<<<grid, kThreads, smem, c.stream>>>(m_up, m_gate, m_x, m_tb, m_lat, a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+    // phase B: y = s W_down (W_down rows are the third part of each neuron record, stride rs).
+    // Prefill (no split) is a compute-bound plain GEMM: cuBLAS.
+    if (!p.split) return gemm_rows_w(blas, nb, L.d, L.F, sb, ld_s, L.w_down, L.rs, y, L.d);
+    if ((e = cudaMemsetAsync(y, 0, sizeof(float) * nb * L.d, c.stream)) != cudaSuccess) return e;
+    DownArgs b;
+    b.d = static_cast<int>(L.d);
+    b.nb = static_cast<int>(nb);
+    b.nbt = p.nbt;
+    b.n_tiles = p.n_tiles;
+    b.kb = static_cast<int>((L.F + kBK - 1) / kBK);
+    b.tiles = static_cast<int>((L.d + kDJ * kBM - 1) / (kDJ * kBM)) * p.n_tiles;
+    b.y = y;
+    const int dcols = 2 * kDJ * p.nbt;  // double-buffered accumulators
+    b.tmem_cols = dcols <= 32 ? 32 : dcols <= 64 ? 64 : dcols <= 128 ? 128 : dcols <= 256 ? 256 : 512;
+    const int brows = 2 * p.nbt;
+    const int dstage = kDJ * kBM * kBK * 2 + brows * kBK * 2;
+    b.stages = static_cast<int>(std::min<size_t>(8, (kMaxDynSmem - fixed) / dstage));
+    if (st_env > 0) b.stages = std::min(b.stages, st_env);
+    const size_t dsmem = fixed + static_cast<size_t>(b.stages) * dstage;
+    CUtensorMap m_w, m_s;
+    // W_down as [F rows (K), d columns (M)]: boxes of 64 columns x 64 rows
+    if (!make_map(&m_w, L.w_down, L.F, L.d, L.rs, kBK) || !make_map(&m_s, sb, p.rows, L.F, ld_s, brows))
+        return cudaErrorInvalidValue;
+    const int64_t dunits = static_cast<int64_t>(b.tiles) * b.kb;
+    int dgrid = static_cast<int>(std::min<int64_t>(std::min(c.num_sms, kMaxCtas), dunits));
+    if (grid_env > 0 && grid_env < dgrid) dgrid = grid_env;
+    if ((e = set_smem(k_tc_down, dsmem)) != cudaSuccess) return e;
+    k_tc_down<<<dgrid, kThreads, dsmem, c.stream>>>(m_w, m_s, b);
+    return cudaGetLastError();
+}
+
+}  // namespace tc
+}  // namespace cdk

@@ -1,0 +1,67 @@
+// kernels_tc.h -- batched decode / prefill on the tensor cores (kernels_tc.cu).
+#pragma once
+
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace cdk {
+namespace tc {
+
+// Arguments of the phase-A kernel (k_tc_gateup).
+struct GateUpArgs {
+    int F = 0, nb = 0;
+    int nbt = 0;        // samples (tokens) per n-tile
+    int N = 0;          // UMMA N: 2 nbt (split) or nbt
+    int kb_x = 0;       // 64-wide k-blocks over d
+    int kb_z = 0;       // 64-wide k-blocks over r (D-CountDown predictor fused), else 0
+    int stages = 0;
+    int tmem_cols = 0;
+    int tiles = 0;      // m-tiles x n-tiles
+    int n_tiles = 0;
+    float* ws = nullptr;        // stream-K partial accumulators, one slot per CTA
+    unsigned* flags = nullptr;  // one release flag per CTA (zero between launches)
+    unsigned long long* tl = nullptr;  // development: per-CTA globaltimer stamps (8 per CTA) or null
+    float tau = 0.0f;
+    const uint8_t* ovr = nullptr;     // nb x F mask override (D-CountDown) or null
+    __nv_bfloat16* s_out = nullptr;   // s rows (pair layout in split mode)
+    int64_t ld_s = 0;
+    uint8_t* mask_out = nullptr;      // nb x F
+    float* ind_out = nullptr;         // nb x F: DC logits, MC u, CATS act(gate), dense u
+    int* alive_out = nullptr;         // nb
+};
+
+// Arguments of the phase-B kernel (k_tc_down).
+struct DownArgs {
+    int d = 0, nb = 0, nbt = 0, n_tiles = 0;
+    int kb = 0;          // 64-neuron k-blocks
+    int tiles = 0;       // j-tiles x n-tiles
+    int stages = 0, tmem_cols = 0;
+    float* y = nullptr;  // nb x d, zeroed; accumulated with red.add
+};
+
+// Tiling of a batch: `split` carries activations as bf16 (hi, lo) pairs (decode); nbt samples per
+// n-tile; rows = B-operand rows of the whole batch (n_tiles x N).
+struct Plan {
+    int split = 1, nbt = 0, N = 0, n_tiles = 0;
+    int64_t rows = 0;
+};
+
+Plan plan_for(int64_t nb, int method);
+size_t workspace_bytes(const LayerDev& L, const Plan& p, int num_sms);
+
+// One batched FFN step: y (nb x d f32) from x (nb x d f32), bf16 weights only.  DC uses the
+// attached predictor (or `ovr`), MC |u| > tau, CATS |act(g)| > tau, dense all rows.
+// `ws` holds workspace_bytes(L, p); `flags` kMaxCtas zero-initialised words (left zero);
+// alive_out is zeroed and accumulated.  Returns
+// cudaErrorInvalidValue for layers it does not cover (f32 weights, missing predictor).
+cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned* flags, cublasHandle_t blas,
+                           int method, int64_t nb,
+                           const float* x, float tau, const uint8_t* ovr, float* y, uint8_t* mask_out,
+                           float* ind_out, int* alive_out, const LaunchCfg& c);
+
+}  // namespace tc
+}  // namespace cdk

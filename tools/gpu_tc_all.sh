@@ -1,0 +1,10 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout -s KILL 400 python -m pytest tests/test_gpu_tc.py -x -q -m gpu 2>&1 | tail -3
+for g in 0; do echo "== grid $g"; CD_TC_GRID=$g timeout -s KILL 200 python tools/tc_timeline.py; done 2>&1 | tee gpurun_out/tc_tl.log
+for g in 0; do echo "== grid $g"; CD_TC_GRID=$g timeout -s KILL 300 python tools/tc_bench.py --steps 20 2>&1 | grep case; done | tee gpurun_out/tc_bench.log
+#!/bin/bash
+mkdir -p gpurun_out
+timeout -s KILL 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file gpurun_out/tc_launches.csv python tools/tc_bench.py --steps 1 --no-graph --cases mc > gpurun_out/tc_ncu.log 2>&1
+echo "ncu rc=$?"

@@ -100,6 +100,15 @@ struct cd_layer {
     bool use_tc = true;     // batches >= kTcMinBatch of a bf16 layer on the tensor cores (CD_TC=0: off)
     cublasHandle_t blas = nullptr;
     Grow tc_ws, blas_ws;    // tensor-core path workspace; cuBLAS workspace (graph-capture safe)
+    // host-call CUDA graph: [H2D inputs, kernels, D2H outputs] replayed while the call signature
+    // (method, batch, tau, options) repeats -- one launch instead of four API calls per step
+    struct HostGraph {
+        uint64_t key = 0;
+        int seen = 0;  // consecutive calls with this key (capture on the second)
+        cudaGraphExec_t exec = nullptr;
+        int launches = 0, path = 0;
+    } hg;
+    bool use_host_graph = true;  // CD_HOST_GRAPH=0 disables
     // large-batch staging (host-buffer calls on the tensor-core path)
     Grow g_dx, g_dy, g_dmask_in, g_dmask_out, g_du_in, g_dind, g_dalive;
     Grow g_hx{true}, g_hy{true}, g_hmask{true}, g_hind{true}, g_halive{true};
@@ -140,6 +149,7 @@ struct cd_layer {
             cudaStreamDestroy(stream);
         }
         if (blas) cublasDestroy(blas);
+        if (hg.exec) cudaGraphExecDestroy(hg.exec);
         for (void* p : dev_allocs) cudaFree(p);
         for (void* p : host_allocs) cudaFreeHost(p);
     }
@@ -388,19 +398,41 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
     float* d_u_in = big ? (io.u_in ? h->g_du_in.get<float>(cf) : nullptr) : h->d_u_in;
     float* d_ind = big ? (io.ind_out ? h->g_dind.get<float>(cf) : nullptr) : h->d_ind;
     float* h_ind = big ? ((io.ind_out || io.u_in) ? h->g_hind.get<float>(cf) : nullptr) : h->h_ind;
+    // single-chunk calls from the fixed staging replay a captured graph of the whole sequence
+    const bool graphable = h->use_host_graph && !big && batch <= chunk;
+    uint64_t key = 0;
+    if (graphable) {
+        uint32_t tau_bits;
+        std::memcpy(&tau_bits, &base.tau, 4);
+        key = (static_cast<uint64_t>(tau_bits) << 32) ^ (static_cast<uint64_t>(batch) << 20) ^
+              (static_cast<uint64_t>(base.method) << 16) ^ (static_cast<uint64_t>(base.reduction) << 12) ^
+              (base.with_masks ? 1u << 8 : 0u) ^ (io.ovr ? 1u << 9 : 0u) ^ (io.masks_in ? 1u << 10 : 0u) ^
+              (io.u_in ? 1u << 11 : 0u) ^ (io.mask_out ? 1u << 5 : 0u) ^ (io.ind_out ? 1u << 6 : 0u) ^ 1u;
+        if (h->hg.key != key) {
+            if (h->hg.exec) cudaGraphExecDestroy(h->hg.exec);
+            h->hg = {};
+            h->hg.key = key;
+        }
+    }
     for (int64_t c0 = 0; c0 < batch; c0 += chunk) {
         const int n = static_cast<int>(std::min<int64_t>(chunk, batch - c0));
         std::memcpy(h_x, io.x + c0 * d, sizeof(float) * n * d);
-        ck(cudaMemcpyAsync(d_x, h_x, sizeof(float) * n * d, cudaMemcpyHostToDevice, s), "H2D x");
         const uint8_t* masks = io.masks_in ? io.masks_in : io.ovr;
-        if (masks) {
-            std::memcpy(h_mask, masks + c0 * F, static_cast<size_t>(n * F));
-            ck(cudaMemcpyAsync(d_mask_in, h_mask, n * F, cudaMemcpyHostToDevice, s), "H2D mask");
-        }
-        if (io.u_in) {
-            std::memcpy(h_ind, io.u_in + c0 * F, sizeof(float) * n * F);
+        if (masks) std::memcpy(h_mask, masks + c0 * F, static_cast<size_t>(n * F));
+        if (io.u_in) std::memcpy(h_ind, io.u_in + c0 * F, sizeof(float) * n * F);
+        const bool replay = graphable && h->hg.exec;
+        const bool capture = graphable && !replay && ++h->hg.seen >= 2;
+        if (replay) {
+            ck(cudaGraphLaunch(h->hg.exec, s), "graph launch");
+            launches += h->hg.launches;
+            h->last_path = h->hg.path;
+        } else {
+        cudaGraph_t graph = nullptr;
+        if (capture) ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+        ck(cudaMemcpyAsync(d_x, h_x, sizeof(float) * n * d, cudaMemcpyHostToDevice, s), "H2D x");
+        if (masks) ck(cudaMemcpyAsync(d_mask_in, h_mask, n * F, cudaMemcpyHostToDevice, s), "H2D mask");
+        if (io.u_in)
             ck(cudaMemcpyAsync(d_u_in, h_ind, sizeof(float) * n * F, cudaMemcpyHostToDevice, s), "H2D u");
-        }
         Req r = base;
         r.nb = n;
         r.x = d_x;
@@ -412,13 +444,38 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
         r.ind_out = io.ind_out ? d_ind : nullptr;
         r.alive_out = d_alive;
         r.stream = s;
-        launches += run_chain(h, r);
-        ck(cudaMemcpyAsync(h_y, d_y, sizeof(float) * n * d, cudaMemcpyDeviceToHost, s), "D2H y");
-        ck(cudaMemcpyAsync(h_alive, d_alive, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "D2H alive");
-        // pinned staging is reused below: the stream sync orders the uploads before the reuse
-        if (io.mask_out) ck(cudaMemcpyAsync(h_mask, d_mask_out, n * F, cudaMemcpyDeviceToHost, s), "D2H mask");
-        if (io.ind_out)
-            ck(cudaMemcpyAsync(h_ind, d_ind, sizeof(float) * n * F, cudaMemcpyDeviceToHost, s), "D2H ind");
+        int nl = 0;
+        try {
+            nl = run_chain(h, r);
+            ck(cudaMemcpyAsync(h_y, d_y, sizeof(float) * n * d, cudaMemcpyDeviceToHost, s), "D2H y");
+            ck(cudaMemcpyAsync(h_alive, d_alive, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "D2H alive");
+            // pinned staging is reused below: the stream sync orders the uploads before the reuse
+            if (io.mask_out) ck(cudaMemcpyAsync(h_mask, d_mask_out, n * F, cudaMemcpyDeviceToHost, s), "D2H mask");
+            if (io.ind_out)
+                ck(cudaMemcpyAsync(h_ind, d_ind, sizeof(float) * n * F, cudaMemcpyDeviceToHost, s), "D2H ind");
+        } catch (...) {
+            if (capture) {
+                cudaStreamEndCapture(s, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                h->use_host_graph = false;
+            }
+            throw;
+        }
+        launches += nl;
+        if (capture) {
+            ck(cudaStreamEndCapture(s, &graph), "capture end");
+            const cudaError_t ie = cudaGraphInstantiate(&h->hg.exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ie != cudaSuccess) {
+                h->hg.exec = nullptr;
+                h->use_host_graph = false;
+                ck(ie, "graph instantiate");
+            }
+            h->hg.launches = nl;
+            h->hg.path = h->last_path;
+            ck(cudaGraphLaunch(h->hg.exec, s), "graph launch");
+        }
+        }
         ck(cudaStreamSynchronize(s), "forward");
         std::memcpy(io.y + c0 * d, h_y, sizeof(float) * n * d);
         if (io.mask_out) std::memcpy(io.mask_out + c0 * F, h_mask, static_cast<size_t>(n * F));
@@ -584,10 +641,11 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     S.t_aux = h->dalloc<unsigned long long>(L.F);
     S.t_count = h->dalloc<unsigned long long>(cdk::kMaxCtas);
     S.t_alive = h->dalloc<unsigned long long>(cdk::kMaxCtas * kMaxBatchFast);
-    S.tc_flags = h->dalloc<unsigned>(cdk::kMaxCtas);
+    S.tc_flags = h->dalloc<unsigned>(cdk::kMaxCtas + 64);
     if (const char* env = std::getenv("CD_DC_CHAIN")) h->use_fused = env[0] != '1';
     if (const char* env = std::getenv("CD_KEEP0")) h->keep0 = std::atoi(env);
     if (const char* env = std::getenv("CD_TC")) h->use_tc = env[0] != '0';
+    if (const char* env = std::getenv("CD_HOST_GRAPH")) h->use_host_graph = env[0] != '0';
     S.ind = h->dalloc<float>(kMaxBatch * L.F);
     S.ex_s = h->dalloc<float>(kMaxBatch * L.F);
     h->d_x = h->dalloc<float>(kMaxBatch * d);

@@ -36,6 +36,13 @@ __device__ __forceinline__ float act_fast(int act, float x) {
     return 0.5f * x * (1.0f + tanhf(inner));
 }
 
+// Tensor-core epilogues (thousands of elements per thread block): SiLU with the hardware exp2 /
+// reciprocal (relative error ~1e-7, far inside the 1e-4 output bound); GeLU-tanh as act_fast.
+__device__ __forceinline__ float act_epi(int act, float x) {
+    if (act == kSilu) return x * __frcp_rn(1.0f + __expf(-x));
+    return act_fast(act, x);
+}
+
 // ---------------------------------------------------------------- vector loads
 // 8 consecutive weights -> 8 floats.  bf16: one 16-byte load; f32: two.
 template <typename W> struct Vec8;

@@ -60,7 +60,7 @@ struct Scratch {
     unsigned long long* t_aux = nullptr;      // F : per-entry payload (M-CountDown: u)
     unsigned long long* t_count = nullptr;    // kMaxCtas : rest-list length per CTA
     unsigned long long* t_alive = nullptr;    // kMaxCtas x kMaxBatchFast : alive counts per CTA
-    unsigned* tc_flags = nullptr;             // kMaxCtas : tensor-core path stream-K flags (zero at rest)
+    unsigned* tc_flags = nullptr;             // kMaxCtas + 64 : tensor-core path flags / counters (zero at rest)
 };
 
 struct LaunchCfg {

@@ -9,20 +9,20 @@
 // fence does: measured 1.5-4.5 us per grid barrier with TMA traffic in flight).
 //
 //   prologue  (before griddepcontrol.wait -- overlaps the previous grid's tail)
-//             producer lane streams this CTA's theta_at slice (its latent columns) and its
-//             theta_bt chunk (its neurons' predictor rows, one contiguous run).
+//             producer lane streams this CTA's theta_at slice (its latent columns); consumers
+//             load their chunk's theta_bt rows into registers (streaming 16-byte loads).
 //   stage 1   latent[q] = theta_at[q] . x for q in this CTA's columns (predictor.cpp:94-102);
 //             each value is published as a tagged word.
 //   stage 2   all CTAs gather the latent (spinning on the tags), s_hat_i = latent . theta_bt[i]
-//             for the chunk's neurons (predictor.cpp:104-113), threshold s_hat > tau_D or the
-//             mask override, CTA-local ballot compaction.  The first K0 active neurons are KEPT
-//             and start streaming at once; the rest are published as tagged list words plus a
-//             tagged per-CTA count.
-//   stage 3   every CTA reads the G counts, and takes ranks c, c+G, c+2G, ... of the concatenated
-//             rest lists (balanced to one record).  A neuron's record [up | gate | down] is ONE
-//             contiguous bulk copy; s_i = up act(gate) (exec_dc blocked_exec.cpp:263-281) and
-//             y += s_i W_down[i] accumulate in registers of the column-owning consumer threads;
-//             one red.global.add.v4 per owned column group at the end.
+//             for the chunk's neurons from registers (predictor.cpp:104-113), threshold
+//             s_hat > tau_D or the mask override, ballot compaction into the own-work list.
+//   stage 3   work stealing: each CTA streams its own actives up to the cap (the previous
+//             launch's active count over the grid), publishes the overflow as tagged queue
+//             entries, and pulls from the launch's queue until the sentinel.  A neuron's record
+//             [up | gate | down] is ONE contiguous bulk copy; s_i = up act(gate) (exec_dc
+//             blocked_exec.cpp:263-281) and y += s_i W_down[i] accumulate in registers of the
+//             column-owning consumer threads; the partial y leaves the CTA in one TMA bulk
+//             reduction.
 //
 // y is zeroed by CTA G-1 (no latent work at the Llama shape) and published by a fence before its
 // count word, which every CTA acquires before its reductions.  The launch tag is read at start

@@ -30,88 +30,12 @@
 #include "kernels.h"
 #include "kernels_tc.h"
 #include "launch.cuh"
+#include "tc_common.cuh"
 
 namespace cdk {
 namespace tc {
 
 namespace {
-
-constexpr int kBM = 128;          // neurons per tile (UMMA M)
-constexpr int kBK = 64;           // K elements per stage: one 128-byte swizzle row of bf16
-constexpr int kEpiWarps = 8;      // two per TMEM lane group, each taking half of the samples
-constexpr int kEpiThreads = 32 * kEpiWarps;
-constexpr int kThreads = 64 + kEpiThreads;  // warp 0 TMA, warp 1 MMA + TMEM owner, then the epilogue
-constexpr int kABytes = kBM * kBK * 2;  // 16 KB per A operand box
-
-// ---------------------------------------------------------------- tcgen05 / TMA primitives
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                            uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-        : "memory");
-}
-
-__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
-}
-
-// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 bytes apart.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
-           (2ull << 61);
-}
-
-// Instruction descriptor, kind::f16: bf16 x bf16 -> f32, both operands K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-           (static_cast<uint32_t>(m >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// 8 consecutive f32 TMEM columns of this thread's lane.
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr)
-                 : "memory");
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
-}
-
-// 16 consecutive f32 TMEM columns of this thread's lane.
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15},"
-        " [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr)
-        : "memory");
-#pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
-}
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------- phase A kernel
 //
@@ -128,38 +52,6 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // the epilogue.  Partials travel through an L2-resident workspace with one release flag per
 // CTA (the finisher resets it: self-cleaning across launches).  Needs all CTAs co-resident
 // (grid <= SMs, one CTA per SM).
-struct Seg {
-    int tile, kb0, kb1;
-};
-
-__device__ __forceinline__ int64_t range_lo(int c, int64_t U, int G) { return static_cast<int64_t>(c) * U / G; }
-
-// Segment `si` of CTA c's range; returns false past the end.
-__device__ __forceinline__ bool seg_at(int c, int si, int64_t U, int G, int nkb, Seg& sg) {
-    const int64_t u1 = range_lo(c + 1, U, G);
-    int64_t u = range_lo(c, U, G);
-    for (int i = 0;; ++i) {
-        if (u >= u1) return false;
-        const int t = static_cast<int>(u / nkb);
-        const int kb0 = static_cast<int>(u - static_cast<int64_t>(t) * nkb);
-        const int kb1 = static_cast<int>((kb0 + (u1 - u) < nkb ? kb0 + (u1 - u) : static_cast<int64_t>(nkb)));
-        if (i == si) {
-            sg = {t, kb0, kb1};
-            return true;
-        }
-        u += kb1 - kb0;
-    }
-}
-
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
 constexpr int kOvr = 4;  // epilogue kind: D-CountDown with a given mask (override / exec_dc)
 
 template <int KIND, bool SPLIT, int ACT>
@@ -427,7 +319,7 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
                         if constexpr (kZ) z += acc[kParts - 1][kH - 1][j];
                     }
                     const bool live = valid && cb + j < nlive;
-                    const float ag = act_fast(ACT, gg);
+                    const float ag = act_epi(ACT, gg);
                     bool on;
                     if constexpr (KIND == kDC) {
                         on = z > a.tau;
@@ -486,11 +378,6 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
 // (128-column j-tile, n-tile), k-blocks 64 neurons; the same stream-K ranges as phase A, each
 // segment's partial reduced into y with red.global.add (TMEM double-buffered: segments do not
 // wait for each other's drain).
-__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr, uint32_t lbo_bytes) {
-    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(lbo_bytes >> 4) << 16) |
-           (64ull << 32) | (1ull << 46) | (2ull << 61);
-}
-
 constexpr int kDJ = 2;  // 128-column j sub-tiles per CTA tile (they share the s tile)
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -682,33 +569,6 @@ __global__ void k_tc_fold_split(const float* __restrict__ in, int64_t ldi, int64
 
 
 // ---------------------------------------------------------------- host: tensor maps, cuBLAS
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    });
-    return fn;
-}
-
-// 2-D bf16 map: `rows` rows of `cols` elements, `stride_elems` apart; boxes of 64 x box_rows,
-// 128-byte swizzle; out-of-range elements read as zero.
-bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t stride_elems, int box_rows) {
-    auto fn = encode_fn();
-    if (!fn) return false;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride_elems * 2)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
-    const cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 cudaError_t cublas_status(cublasStatus_t s) { return s == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown; }
 
 // Row-major C (rows x n, ldc) = A (rows x k, lda) * W, W k x n row-major (ldw).
@@ -759,6 +619,13 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
                            float* ind_out, int* alive_out, const LaunchCfg& c) {
     if (L.dtype != 1 /* bf16 */ || !L.w_up) return cudaErrorInvalidValue;
     if (method == kDC && !ovr && !L.theta_bt) return cudaErrorInvalidValue;
+    static const bool fused_env = [] {
+        const char* e = std::getenv("CD_TC_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    if (p.split && fused_env)
+        return launch_batched_fused(L, p, ws, workspace_bytes(L, p, c.num_sms), flags, method, nb, x, tau, ovr, y,
+                                    mask_out, ind_out, alive_out, c);
     const int64_t ldr = L.ldr > 0 ? L.ldr : 8;
     const int64_t ld_s = round_up64(L.F, 8);
     uint8_t* w = static_cast<uint8_t*>(ws);

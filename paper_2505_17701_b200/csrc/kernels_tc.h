@@ -63,5 +63,11 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
                            const float* x, float tau, const uint8_t* ovr, float* y, uint8_t* mask_out,
                            float* ind_out, int* alive_out, const LaunchCfg& c);
 
+// The same step (split mode only) as ONE persistent kernel (kernels_tc_fused.cu): latent,
+// gate/up + masks, down.  `ws` of ws_bytes (workspace_bytes); flags: kMaxCtas + 4 zeroed words.
+cudaError_t launch_batched_fused(const LayerDev& L, const Plan& p, void* ws, size_t ws_bytes, unsigned* flags,
+                                 int method, int64_t nb, const float* x, float tau, const uint8_t* ovr, float* y,
+                                 uint8_t* mask_out, float* ind_out, int* alive_out, const LaunchCfg& c);
+
 }  // namespace tc
 }  // namespace cdk

@@ -30,9 +30,12 @@ for method in (_capi.METHOD_MC, _capi.METHOD_DC):
     t0 = t[:, 0].min()
     rel = np.where(t > 0, (t - t0) / 1e3, np.nan)
     print("method", method, "CTAs", n)
-    for k, name in enumerate(["start", "tma0", "mma_end", "epi0", "epi1", "epi2", "epi_end", "exit"]):
+    names = (["start", "mmaA_end", "prod_swait", "prod_sgo", "epiA_end", "epiB_end", "fin_flags", "fin_start"]
+             if os.environ.get("CD_TC_FUSED", "1") != "0" else
+             ["start", "tma0", "mma_end", "epi0", "epi1", "epi2", "epi_end", "exit"])
+    for k, name in enumerate(names):
         col = rel[:, k]
         if np.all(np.isnan(col)):
             continue
         print(f"  {name:8s} min {np.nanmin(col):7.2f}  med {np.nanmedian(col):7.2f}  max {np.nanmax(col):7.2f}")
-    print("  slowest CTAs (exit):", np.argsort(-np.nan_to_num(rel[:, 7]))[:8].tolist())
+

@@ -109,6 +109,7 @@ struct cd_layer {
         int launches = 0, path = 0;
     } hg;
     bool use_host_graph = true;  // CD_HOST_GRAPH=0 disables
+    bool mapped_staging = true;  // fixed pinned staging is device-addressable (copy kernels)
     // large-batch staging (host-buffer calls on the tensor-core path)
     Grow g_dx, g_dy, g_dmask_in, g_dmask_out, g_du_in, g_dind, g_dalive;
     Grow g_hx{true}, g_hy{true}, g_hmask{true}, g_hind{true}, g_halive{true};
@@ -138,7 +139,14 @@ struct cd_layer {
     }
     template <typename T> T* halloc(size_t n) {
         void* p = nullptr;
-        ck(cudaMallocHost(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMallocHost");
+        // mapped: the copy kernels of the host-buffer calls read / write it directly (UVA: the
+        // device address is the host address; otherwise those calls use the DMA engine)
+        ck(cudaHostAlloc(&p, std::max<size_t>(n, 1) * sizeof(T), cudaHostAllocMapped), "cudaHostAlloc");
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, p, 0) != cudaSuccess || dp != p) {
+            (void)cudaGetLastError();
+            mapped_staging = false;
+        }
         host_allocs.push_back(p);
         return static_cast<T*>(p);
     }
@@ -429,10 +437,16 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
         } else {
         cudaGraph_t graph = nullptr;
         if (capture) ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
-        ck(cudaMemcpyAsync(d_x, h_x, sizeof(float) * n * d, cudaMemcpyHostToDevice, s), "H2D x");
-        if (masks) ck(cudaMemcpyAsync(d_mask_in, h_mask, n * F, cudaMemcpyHostToDevice, s), "H2D mask");
-        if (io.u_in)
-            ck(cudaMemcpyAsync(d_u_in, h_ind, sizeof(float) * n * F, cudaMemcpyHostToDevice, s), "H2D u");
+        // small transfers from the fixed (mapped) pinned staging: a copy kernel, not the DMA engine
+        auto xfer = [&](void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, const char* what) {
+            if (!big && h->mapped_staging && bytes <= (size_t{1} << 20))
+                ck(cdk::launch_copy(dst, src, bytes, s), what);
+            else
+                ck(cudaMemcpyAsync(dst, src, bytes, kind, s), what);
+        };
+        xfer(d_x, h_x, sizeof(float) * n * d, cudaMemcpyHostToDevice, "H2D x");
+        if (masks) xfer(d_mask_in, h_mask, static_cast<size_t>(n * F), cudaMemcpyHostToDevice, "H2D mask");
+        if (io.u_in) xfer(d_u_in, h_ind, sizeof(float) * n * F, cudaMemcpyHostToDevice, "H2D u");
         Req r = base;
         r.nb = n;
         r.x = d_x;
@@ -447,12 +461,11 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
         int nl = 0;
         try {
             nl = run_chain(h, r);
-            ck(cudaMemcpyAsync(h_y, d_y, sizeof(float) * n * d, cudaMemcpyDeviceToHost, s), "D2H y");
-            ck(cudaMemcpyAsync(h_alive, d_alive, sizeof(int) * n, cudaMemcpyDeviceToHost, s), "D2H alive");
+            xfer(h_y, d_y, sizeof(float) * n * d, cudaMemcpyDeviceToHost, "D2H y");
+            xfer(h_alive, d_alive, sizeof(int) * n, cudaMemcpyDeviceToHost, "D2H alive");
             // pinned staging is reused below: the stream sync orders the uploads before the reuse
-            if (io.mask_out) ck(cudaMemcpyAsync(h_mask, d_mask_out, n * F, cudaMemcpyDeviceToHost, s), "D2H mask");
-            if (io.ind_out)
-                ck(cudaMemcpyAsync(h_ind, d_ind, sizeof(float) * n * F, cudaMemcpyDeviceToHost, s), "D2H ind");
+            if (io.mask_out) xfer(h_mask, d_mask_out, static_cast<size_t>(n * F), cudaMemcpyDeviceToHost, "D2H mask");
+            if (io.ind_out) xfer(h_ind, d_ind, sizeof(float) * n * F, cudaMemcpyDeviceToHost, "D2H ind");
         } catch (...) {
             if (capture) {
                 cudaStreamEndCapture(s, &graph);
@@ -646,6 +659,7 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     if (const char* env = std::getenv("CD_KEEP0")) h->keep0 = std::atoi(env);
     if (const char* env = std::getenv("CD_TC")) h->use_tc = env[0] != '0';
     if (const char* env = std::getenv("CD_HOST_GRAPH")) h->use_host_graph = env[0] != '0';
+    if (const char* env = std::getenv("CD_COPY_KERNEL")) h->mapped_staging = h->mapped_staging && env[0] != '0';
     S.ind = h->dalloc<float>(kMaxBatch * L.F);
     S.ex_s = h->dalloc<float>(kMaxBatch * L.F);
     h->d_x = h->dalloc<float>(kMaxBatch * d);

@@ -134,6 +134,9 @@ cudaError_t launch_exact_act(int act, float* v, int64_t n, const LaunchCfg& c);
 cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,
                               const LaunchCfg& c);
 
+// dst[0, bytes) = src[0, bytes) by a kernel (either side may be mapped pinned host memory).
+cudaError_t launch_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 // One-thread kernel that occupies the stream for `ns` nanoseconds (timing helper).
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t s);
 

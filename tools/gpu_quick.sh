@@ -1,5 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout -s KILL 900 python -m pytest tests -x -q -m gpu --timeout 300 2>&1 | tail -3
-timeout -s KILL 600 python bench.py --no-sweep --no-batched --no-cpu-baseline > gpurun_out/quick_bench.json 2> gpurun_out/quick_bench.err
-python -c "import json; d=json.load(open('gpurun_out/quick_bench.json')); print(d['value'], d['e2e'])"
+timeout -s KILL 300 python tools/e2e_probe.py 2>&1 | head -2
+CD_COPY_KERNEL=0 timeout -s KILL 300 python tools/e2e_probe.py 2>&1 | head -1
+CD_HOST_GRAPH=0 timeout -s KILL 300 python tools/e2e_probe.py 2>&1 | head -1
+timeout -s KILL 900 python -m pytest tests -x -q -m gpu --timeout 300 2>&1 | tail -2
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()"

@@ -244,6 +244,26 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
             }
         }
         pdl_wait();  // y and the scratch words of the previous step are now safe to touch
+        // x into registers right away (column ownership: vectors ct + j*nc), in flight together
+        // with thread 0's launch-tag / queue-word reads below.  Plain vector loads, not the TMA
+        // engine: a bulk copy of x would queue behind this CTA's predictor prefetch.
+        float xr[NB][VPT][8];
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int vec = ct + j * nc;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+                const int64_t col = (int64_t)vec * kVec;
+                if (vec < nvec && b < nb) {
+                    const float4* src = reinterpret_cast<const float4*>(x + b * L.d + col);
+                    if (col < L.d) lo = __ldcg(src);
+                    if (col + 4 < L.d) hi = __ldcg(src + 1);
+                }
+                xr[b][j][0] = lo.x; xr[b][j][1] = lo.y; xr[b][j][2] = lo.z; xr[b][j][3] = lo.w;
+                xr[b][j][4] = hi.x; xr[b][j][5] = hi.y; xr[b][j][6] = hi.z; xr[b][j][7] = hi.w;
+            }
+        }
         if (threadIdx.x == 0) {
             TL(5, 1);
             const uint32_t t = static_cast<uint32_t>(__ldcg(S.ctl + kCtlEpoch)) + 1u;
@@ -268,25 +288,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         }
         named_bar_sync(kBarC, nc);
         const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
-        // x into registers (column ownership: vectors ct + j*nc).  Plain vector loads, not the
-        // TMA engine: a bulk copy of x would queue behind this CTA's predictor prefetch.
-        float xr[NB][VPT][8];
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            const int vec = ct + j * nc;
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
-                const int64_t col = (int64_t)vec * kVec;
-                if (vec < nvec && b < nb) {
-                    const float4* src = reinterpret_cast<const float4*>(x + b * L.d + col);
-                    if (col < L.d) lo = __ldcg(src);
-                    if (col + 4 < L.d) hi = __ldcg(src + 1);
-                }
-                xr[b][j][0] = lo.x; xr[b][j][1] = lo.y; xr[b][j][2] = lo.z; xr[b][j][3] = lo.w;
-                xr[b][j][4] = hi.x; xr[b][j][5] = hi.y; xr[b][j][6] = hi.z; xr[b][j][7] = hi.w;
-            }
-        }
         if (threadIdx.x == 0) TL(6, 2);
 
         // ---------------------------------------------------------- stage 1: latent columns

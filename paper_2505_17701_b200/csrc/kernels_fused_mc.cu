@@ -18,6 +18,11 @@
 //
 // y zeroing, the launch tag and the per-CTA alive counts work as in kernels_fused.cu
 // (fused_common.cuh).  Grid == number of SMs, one CTA per SM, all CTAs co-resident.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fused_common.cuh"
 #include "kernels.h"
@@ -39,6 +44,8 @@ struct MetaM {
 };
 
 struct FusedMcParams {
+    CUtensorMap wu_map;  // W_up as [rows (stride rs)][ld / inner][inner]: one box = 3 whole rows
+    int use_map;
     LayerDev L;
     Scratch S;
     const float* x;
@@ -48,7 +55,25 @@ struct FusedMcParams {
     int* alive_out;
     float tau;
     int nstages, rows_per_cta, rows_per_stage;
+    unsigned long long* tl;  // development (CD_MC_TL): per-CTA globaltimer stamps, 8 per CTA
 };
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void mstamp(const FusedMcParams& P, int k) {
+    if (P.tl) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.tl[blockIdx.x * 8 + k] = t;
+    }
+}
 
 template <typename W, int VPT>
 __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ FusedMcParams P) {
@@ -91,6 +116,7 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
     }
     __syncthreads();
     pdl_launch_dependents();
+    if (threadIdx.x == 0) mstamp(P, 0);
 
     const W* WU = static_cast<const W*>(L.w_up);
     const W* WG = static_cast<const W*>(L.w_gate);  // [gate | down] of neuron i at WG + i * rs
@@ -107,10 +133,17 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
                 const int64_t r0 = c0 + (int64_t)s * rps;
                 const int n = static_cast<int>(imin64(rps, c1 - r0));
                 mbar_wait(&empty[st], ph ^ 1);
-                mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(n * row_bytes));
-                for (int q = 0; q < n; ++q)
-                    bulk_g2s(ring + st * stage_bytes + q * row_bytes, WU + (r0 + q) * L.rs,
-                             static_cast<uint32_t>(row_bytes), &full[st], pol);
+                if (P.use_map) {
+                    // one tensor copy for the stage's rows (the box always carries rps rows; rows
+                    // past the chunk are read but unused, past F zero-filled)
+                    mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rps * row_bytes));
+                    tma_load_3d(ring + st * stage_bytes, &P.wu_map, 0, 0, static_cast<int>(r0), &full[st], pol);
+                } else {
+                    mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(n * row_bytes));
+                    for (int q = 0; q < n; ++q)
+                        bulk_g2s(ring + st * stage_bytes + q * row_bytes, WU + (r0 + q) * L.rs,
+                                 static_cast<uint32_t>(row_bytes), &full[st], pol);
+                }
                 if (++st == nstages) { st = 0; ph ^= 1; }
             }
         }
@@ -215,44 +248,58 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
         }
 
         // ---------------------------------------------------------- stage 1: u = W_up x, threshold
+        // Stages are consumed (and handed back to the producer) one by one, but reduced across
+        // warps in groups of kSG stages: one CTA barrier per 3 kSG rows instead of per 3.
+        constexpr int kSG = 4;
         int st = 0;
         uint32_t ph = 0;
-        for (int s = 0; s < nst_u; ++s) {
-            const int64_t r0 = c0 + (int64_t)s * rps;
-            const int n = static_cast<int>(imin64(rps, c1 - r0));
-            mbar_wait(&full[st], ph);
-            const W* base = reinterpret_cast<const W*>(ring + st * stage_bytes);
-            float v[4];
+        for (int s0 = 0, grp = 0; s0 < nst_u; s0 += kSG, ++grp) {
+            float v[4 * kSG];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                float a0 = 0.0f, a1 = 0.0f;
-                if (q < n) {
+            for (int g = 0; g < kSG; ++g) {
+                const int s = s0 + g;
 #pragma unroll
-                    for (int j = 0; j < VPT; ++j) {
-                        const int vec = ct + j * nc;
-                        if (vec < nvec) {
-                            float w[8];
-                            Vec8<W>::load(base + q * L.ld + vec * kVec, w);
+                for (int q = 0; q < 4; ++q) v[g * 4 + q] = 0.0f;
+                if (s < nst_u) {
+                    const int n = static_cast<int>(imin64(rps, c1 - (c0 + (int64_t)s * rps)));
+                    mbar_wait(&full[st], ph);
+                    if (s == 0 && threadIdx.x == 0) mstamp(P, 1);
+                    const W* base = reinterpret_cast<const W*>(ring + st * stage_bytes);
 #pragma unroll
-                            for (int k = 0; k < 8; k += 2) ffma2(a0, a1, w[k], w[k + 1], xr[j][k], xr[j][k + 1]);
+                    for (int q = 0; q < 3; ++q) {
+                        float a0 = 0.0f, a1 = 0.0f;
+                        if (q < n) {
+#pragma unroll
+                            for (int j = 0; j < VPT; ++j) {
+                                const int vec = ct + j * nc;
+                                if (vec < nvec) {
+                                    float w[8];
+                                    Vec8<W>::load(base + q * L.ld + vec * kVec, w);
+#pragma unroll
+                                    for (int k = 0; k < 8; k += 2) ffma2(a0, a1, w[k], w[k + 1], xr[j][k], xr[j][k + 1]);
+                                }
+                            }
                         }
+                        v[g * 4 + q] = a0 + a1;
                     }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[st]);  // stage data consumed: the producer refills it
+                    if (++st == nstages) { st = 0; ph ^= 1; }
                 }
-                v[q] = a0 + a1;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);  // stage data consumed: the producer refills it
-            if (++st == nstages) { st = 0; ph ^= 1; }
-            const float tot = warp_transpose_sum<4>(v);
-            float* rb = red + (s & 1) * nwc * 4;  // double-buffered: one barrier per stage
-            if ((lane & 7) == 0) rb[warp * 4 + (lane >> 3)] = tot;
+            const float tot = warp_transpose_sum<4 * kSG>(v);
+            float* rb = red + (grp & 1) * nwc * 16;  // double-buffered: one barrier per group
+            if ((lane & 1) == 0) rb[warp * 16 + (lane >> 1)] = tot;
             named_bar_sync(kBarC, nc);
             if (warp == 0) {
-                const bool valid = lane < n;
+                // lane l: row q = l % 4 of stage s0 + l / 4
+                const int s = s0 + (lane >> 2), q = lane & 3;
+                const int64_t r0 = c0 + (int64_t)s * rps;
+                const bool valid = lane < 4 * kSG && s < nst_u && q < 3 && r0 + q < c1;
                 float u = 0.0f;
                 if (valid)
-                    for (int w = 0; w < nwc; ++w) u += rb[w * 4 + lane];
-                const int64_t gi = r0 + lane;
+                    for (int w = 0; w < nwc; ++w) u += rb[w * 16 + lane];
+                const int64_t gi = r0 + q;
                 bool a = false;
                 if (valid) {
                     a = fabsf(u) > P.tau;
@@ -271,6 +318,7 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
             }
         }
         named_bar_sync(kBarC, nc);
+        if (threadIdx.x == 0) mstamp(P, 2);
         named_bar_arrive(kBarK, nc + kWarp);  // producer may schedule stage 3 now
         if (threadIdx.x == 0) {
             st_relaxed_u64(S.t_alive + blockIdx.x * kMaxBatchFast, tagged(tag, static_cast<uint32_t>(cnt[0])));
@@ -295,6 +343,7 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
                 if (!done) {
                     mbar_wait(&full[st], ph);
                     if (meta[st].idx < 0) done = true;
+                    if (n_rec == 0 && q == 0 && threadIdx.x == 0) mstamp(P, 3);
                 }
                 if (!done) {
                     ns = q + 1;
@@ -348,6 +397,7 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
                 }
             }
         }
+        if (threadIdx.x == 0) mstamp(P, 4);
         if (n_rec > 0) {
             named_bar_sync(kBarC, nc);  // every consumer is past its last ring read
             float* ys = reinterpret_cast<float*>(ring);
@@ -367,6 +417,7 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
                 bulk_commit_and_wait_read();
             }
         }
+        if (threadIdx.x == 0) mstamp(P, 5);
         if (blockIdx.x == 0 && warp == 0) {
             if (P.alive_out) {
                 int a = 0;
@@ -419,6 +470,41 @@ cudaError_t launch_mc_fused(const LayerDev& L, const Scratch& S, const float* x,
         p.nstages = nstages;
         p.rows_per_cta = rpc;
         p.rows_per_stage = 3;
+        // W_up stage loads as one 3-D tensor copy: [rows][ld / inner][inner], no swizzle (the smem
+        // image is the plain row-major 3 x ld block the consumers read)
+        p.use_map = 0;
+        static const bool map_env = [] {
+            const char* e = std::getenv("CD_MC_TMAP");
+            return !(e && e[0] == '0');
+        }();
+        int inner = 0;
+        for (int cand : {256, 128, 64, 32, 16, 8})
+            if (L.ld % cand == 0 && L.ld / cand <= 256) { inner = cand; break; }
+        static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+            void* fp = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            return (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+                    q == cudaDriverEntryPointSuccess)
+                       ? reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp)
+                       : nullptr;
+        }();
+        if (map_env && inner > 0 && enc) {
+            const cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(L.ld / inner),
+                                        static_cast<cuuint64_t>(L.F)};
+            const cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner * esz), static_cast<cuuint64_t>(L.rs * esz)};
+            const cuuint32_t box[3] = {static_cast<cuuint32_t>(inner), static_cast<cuuint32_t>(L.ld / inner), 3u};
+            const cuuint32_t estr[3] = {1, 1, 1};
+            if (enc(&p.wu_map, L.dtype == kBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                    const_cast<void*>(L.w_up), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                p.use_map = 1;
+        }
+        static unsigned long long* tl_env = [] {
+            const char* e = std::getenv("CD_MC_TL");
+            return e ? reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 10)) : nullptr;
+        }();
+        p.tl = tl_env;
         return launch_ex(kern, dim3(G), dim3(threads), smem, c, true, p);
     };
     if (L.dtype == kBF16) {

@@ -31,6 +31,7 @@
 //
 // Requirements: grid == number of SMs, one CTA per SM (the dynamic shared memory forces it), all
 // CTAs co-resident (the spins wait on other CTAs).
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -65,6 +66,7 @@ struct FusedParams {
     int* alive_out;
     float tau;
     int nb, nstages, rows_per_cta, keep0, qrows;
+    int b_smem;  // bf16: predictor rows staged by TMA in the ring, moved to registers after stage 1
 };
 
 template <typename W, int NB, int VPT, int VPL>
@@ -150,7 +152,8 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
                 mbar_arrive_expect_tx(bar_a, static_cast<uint32_t>(nq * arow_bytes));
                 bulk_g2s(abuf, AT + (int64_t)q0 * L.ld, static_cast<uint32_t>(nq * arow_bytes), bar_a, pol);
             }
-            if (!kRegB && nrows > 0) {
+            if ((!kRegB || P.b_smem) && nrows > 0) {
+                // the chunk's predictor rows: one bulk copy into the (idle) ring head
                 const int64_t bytes = nrows * brow_bytes;
                 mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bytes));
                 bulk_g2s(ring, BT + c0 * brow_bytes, static_cast<uint32_t>(bytes), bar_b, pol);
@@ -230,7 +233,10 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         // register path: this warp's predictor rows (warp + i*nwc of the chunk), lane owns
         // vectors lane + v*32 of each row -- coalesced 16-byte loads, weights only
         uint4 rb[kRegB ? kRowsW : 1][VPL];
-        if constexpr (kRegB) {
+        if (kRegB && !P.b_smem) {
+            // (b_smem: the rows arrive by TMA and are moved to registers after stage 1 instead --
+            // 8 K register loads here would delay a late-starting CTA's griddepcontrol.wait,
+            // and with it its latent columns that every CTA gathers)
             const W* BTw = static_cast<const W*>(L.theta_bt);
 #pragma unroll
             for (int i = 0; i < kRowsW; ++i) {
@@ -334,6 +340,22 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
             }
         }
         if (threadIdx.x == 0) TL(5, 2);
+        if (kRegB && P.b_smem) {
+            // predictor rows smem -> registers while the latent columns of the other CTAs arrive
+            if (nrows > 0) mbar_wait(bar_b, 0);
+            const int nvr_b = static_cast<int>(L.ldr / kVec);
+#pragma unroll
+            for (int i = 0; i < kRowsW; ++i) {
+                const int rl = warp + i * nwc;
+#pragma unroll
+                for (int v = 0; v < VPL; ++v) {
+                    const int vec = lane + v * kWarp;
+                    rb[i][v] = make_uint4(0u, 0u, 0u, 0u);
+                    if (rl < nrows && vec < nvr_b)
+                        rb[i][v] = *reinterpret_cast<const uint4*>(ring + rl * brow_bytes + vec * 16);
+                }
+            }
+        }
 
         // ---------------------------------------------------------- stage 2: predictor + compaction
         // gather the latent (every CTA published its columns as tagged words): all of a thread's
@@ -726,6 +748,11 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
     const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
     if (nstages < 2) return cudaErrorInvalidValue;
+    static const bool bsmem_env = [] {
+        const char* e = std::getenv("CD_DC_BSMEM");
+        return !(e && e[0] == '0');
+    }();
+    const int b_smem = regb && bsmem_env && (int64_t)rpc * brow_bytes + aux_bytes <= stage_bytes * nstages ? 1 : 0;
     if (regb ? rpc > nwc * 8 : (int64_t)rpc * brow_bytes + aux_bytes > stage_bytes * nstages)
         return cudaErrorInvalidValue;  // register path: <= 8 predictor rows per consumer warp
     if (aux_bytes > stage_bytes * nstages) return cudaErrorInvalidValue;
@@ -748,6 +775,7 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
         p.rows_per_cta = rpc;
         p.keep0 = keep0;
         p.qrows = qrows;
+        p.b_smem = b_smem;
         return launch_ex(kern, dim3(G), dim3(threads), smem, c, true, p);
     };
 #define CD_FUSED_CASES(W)                                          \

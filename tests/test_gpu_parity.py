@@ -419,3 +419,25 @@ def test_gpu_calibration_matches_reference(oracle, reference):
     m = cd.alive_count_for(0.8, 256)
     want = np.mean([float(np.sort(z)[::-1][m]) for z in zs])
     assert abs(tau - want) <= 1e-6 * max(1.0, abs(want))
+
+
+def test_host_call_graph_replay_and_recapture(oracle):
+    """Host-buffer calls replay a per-handle CUDA graph while (method, batch, tau, options) repeat
+    (capture on the second identical call) and recapture when they change; results stay equal to
+    the oracle on every call, with fresh inputs each time."""
+    g, layer, pred = make_case(oracle, 106, 512, 2048, 64, 0, "bf16")
+    _, z0 = oracle.lowrank_logits(g["theta_a"], g["theta_b"], g["x"])
+    rng = oracle.rng(11)
+    for tau in (float(np.quantile(z0, 0.8)), float(np.quantile(z0, 0.5)), float(np.quantile(z0, 0.8))):
+        for _ in range(4):
+            x = rng.normals_f(512)
+            got = cd.pipeline_dc(layer, x, pred, FAST, tau_d=tau, want_logits=True)
+            _, z = oracle.lowrank_logits(g["theta_a"], g["theta_b"], x)
+            check_mask_flips(got.mask.alive, (z > tau).astype(np.uint8), z, tau, 1e-4)
+            assert got.mask.alive_count == int(got.mask.alive.sum())
+            assert rel_l2(got.y, oracle.forward_sparse(g, x, got.mask.alive)) <= 1e-4
+            # interleave another method / batch on the same handle (a different graph key)
+            X = np.stack([rng.normals_f(512) for _ in range(2)])
+            yd = cd.exec_dense(layer, X, FAST)
+            for b in range(2):
+                assert rel_l2(yd[b], oracle.forward_dense(g, X[b])["y"]) <= 1e-4

@@ -73,6 +73,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256) red_cluster(flo
     }
 }
 
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+// E: each CTA stages its 16 KB partial in smem and issues ONE bulk reduction into y (the fused
+// decode kernel's epilogue)
+__global__ void __launch_bounds__(256) bulk_all(float* y) {
+    __shared__ __align__(128) float ys[D];
+    const int t = threadIdx.x;
+    if (t == 0) g_t[0][blockIdx.x] = gtime();
+    for (int i = t; i < D; i += 256) ys[i] = 1.f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (t == 0) {
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(y),
+                     "r"(smem_addr(ys)), "r"(D * 4) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        g_t[1][blockIdx.x] = gtime();
+    }
+}
+
+// F: 2-CTA clusters: rank 1 adds its partial into rank 0's smem over DSMEM, rank 0 bulk-reduces
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256) bulk_cluster(float* y) {
+    __shared__ __align__(128) float ys[D];
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();
+    const int t = threadIdx.x;
+    if (t == 0) g_t[0][blockIdx.x] = gtime();
+    for (int i = t; i < D; i += 256) ys[i] = 1.f;
+    cl.sync();
+    if (rank == 1) {
+        float* peer = cl.map_shared_rank(ys, 0);
+        for (int i = t * 4; i < D; i += 256 * 4) {
+            const float4 v = *reinterpret_cast<const float4*>(ys + i);
+            atomicAdd(peer + i, v.x);
+            atomicAdd(peer + i + 1, v.y);
+            atomicAdd(peer + i + 2, v.z);
+            atomicAdd(peer + i + 3, v.w);
+        }
+    }
+    cl.sync();
+    if (rank == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(y),
+                         "r"(smem_addr(ys)), "r"(D * 4) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+    }
+    if (t == 0) g_t[1][blockIdx.x] = gtime();
+}
+
 __global__ void __launch_bounds__(256) empty_k(float* y) {
     if (threadIdx.x == 0) { g_t[0][blockIdx.x] = gtime(); __threadfence(); g_t[1][blockIdx.x] = gtime(); }
 }
@@ -116,6 +169,8 @@ int main() {
     time_it("D 8 copies", [&] { red_all<<<nsm, 256>>>(y, 0, 8); });
     time_it("D 8 copies rotated", [&] { red_all<<<nsm, 256>>>(y, 1, 8); });
     time_it("C 2-CTA cluster DSMEM halves", [&] { red_cluster<<<nsm, 256>>>(y); });
+    time_it("E bulk reduce 16 KB per CTA -> one y", [&] { bulk_all<<<nsm, 256>>>(y); });
+    time_it("F 2-CTA cluster DSMEM add + bulk reduce", [&] { bulk_cluster<<<nsm, 256>>>(y); });
     CK(cudaGetLastError());
     return 0;
 }

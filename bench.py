@@ -257,14 +257,18 @@ def run_reference(args):
         taus.append(float(z[order[m]]))
     tau = float(np.mean(taus))
     masks = [(ref.predict_logits(g["theta_a"], g["theta_b"], x) > np.float32(tau)).astype(np.uint8) for x in xs]
+    # the reference layer / predictor objects are built once (as its own bench() does,
+    # blocked_exec.cpp:396-415); each timed step is one pipeline_dc call
+    h = ref.model(g)
     for i in range(args.warmup):
-        ref.pipeline_dc(g, xs[i % N_X], masks[i % N_X])
+        ref.model_pipeline_dc(h, xs[i % N_X], D, masks[i % N_X])
     t0 = time.perf_counter()
     alive = 0
     for i in range(args.steps):
-        r = ref.pipeline_dc(g, xs[i % N_X], masks[i % N_X])
+        r = ref.model_pipeline_dc(h, xs[i % N_X], D, masks[i % N_X])
         alive += r["alive"]
     dt = time.perf_counter() - t0
+    ref.model_free(h)
     v = args.steps / dt
     cores = ref.max_threads()
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,

@@ -289,6 +289,10 @@ class Reference:
         L.ref_pipeline_dc.argtypes = [_i64, _i64, _i64, C.c_int, _f32p, _f32p, _f32p, _f32p, _f32p,
                                       _f32p, vp, _i64, _i64, C.c_int, _f32p, _u8p, C.POINTER(_i64),
                                       _i64p]
+        L.ref_model_new.argtypes = [_i64, _i64, _i64, C.c_int, _f32p, _f32p, _f32p, _f32p, _f32p,
+                                    C.POINTER(vp)]
+        L.ref_model_free.argtypes = [vp]
+        L.ref_model_pipeline_dc.argtypes = [vp, _f32p, vp, _i64, _i64, C.c_int, _f32p, C.POINTER(_i64)]
         L.ref_bench.argtypes = [C.c_int, _i64, _i64, _i64, C.c_double, _i64, _i64, _i64, C.c_int,
                                 _u64, _i64p, C.POINTER(C.c_double)]
         L.ref_bench_reference_dense.argtypes = [_i64, _i64, _i64, _u64, _i64p]
@@ -422,6 +426,26 @@ class Reference:
                                          L["theta_a"], L["theta_b"], x, _opt(mo), blk[0], blk[1],
                                          reduction, y, mask, C.byref(alive), t))
         return dict(y=y, mask=mask, alive=int(alive.value), traffic=tuple(int(v) for v in t))
+
+    def model(self, L, act=0):
+        """A persistent reference GatedMlpLayer + low-rank Predictor (for timed loops)."""
+        F, d = L["w_up"].shape
+        r = L["theta_a"].shape[1]
+        h = C.c_void_p()
+        self._chk(self.L.ref_model_new(d, F, r, act, L["w_up"], L["w_gate"], L["w_down"], L["theta_a"],
+                                       L["theta_b"], C.byref(h)))
+        return h
+
+    def model_free(self, h):
+        self.L.ref_model_free(h)
+
+    def model_pipeline_dc(self, h, x, d, mask_override=None, blk=(16, 256), reduction=0):
+        y = np.empty(d, np.float32)
+        alive = _i64()
+        mo = None if mask_override is None else np.ascontiguousarray(mask_override, np.uint8)
+        self._chk(self.L.ref_model_pipeline_dc(h, np.ascontiguousarray(x, np.float32), _opt(mo), blk[0], blk[1],
+                                               reduction, y, C.byref(alive)))
+        return dict(y=y, alive=int(alive.value))
 
     def bench(self, method: str, d, F, r, k, iters, seed=42, blk=(16, 256), reduction=0):
         m = {"dense": 0, "cats": 1, "mc": 2, "dc": 3}[method]

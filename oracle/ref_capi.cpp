@@ -284,6 +284,39 @@ int ref_pipeline_dc(int64_t d, int64_t F, int64_t rank, int act, const float* up
     });
 }
 
+// A persistent reference layer + predictor (built once), so a timed loop measures pipeline_dc
+// itself rather than the construction of a 700 MB GatedMlpLayer from raw arrays per call.
+struct RefModel {
+    GatedMlpLayer layer;
+    Predictor pred;
+};
+
+int ref_model_new(int64_t d, int64_t F, int64_t rank, int act, const float* up, const float* gate,
+                  const float* down, const float* ta, const float* tb, void** out) {
+    return guarded([&] {
+        *out = new RefModel{layer_of(d, F, act, up, gate, down), predictor_of(d, rank, F, ta, tb)};
+    });
+}
+
+int ref_model_free(void* h) {
+    delete static_cast<RefModel*>(h);
+    return 0;
+}
+
+int ref_model_pipeline_dc(void* h, const float* x, const uint8_t* mask_override, int64_t blk_m, int64_t blk_n,
+                          int reduction, float* y, int64_t* alive) {
+    return guarded([&] {
+        const RefModel& m = *static_cast<const RefModel*>(h);
+        const int64_t d = m.layer.d_model, F = m.layer.d_inter;
+        ActivationMask ov;
+        if (mask_override) ov = mask_of(F, mask_override);
+        PipelineResult r = pipeline_dc(m.layer, vec(x, d), m.pred, cfg_of(blk_m, blk_n, reduction),
+                                       mask_override ? &ov : nullptr);
+        put(r.y, y);
+        if (alive) *alive = r.mask.alive_count;
+    });
+}
+
 // method: 0 dense, 1 cats, 2 mc, 3 dc.  out: p50_ns, p95_ns, traffic_elements; ratio.
 int ref_bench(int method, int64_t d, int64_t F, int64_t r, double k, int64_t iters,
               int64_t blk_m, int64_t blk_n, int reduction, uint64_t seed, int64_t* out3,

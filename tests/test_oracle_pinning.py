@@ -179,3 +179,17 @@ def test_reference_unit_tests_pass():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "0 failed" in r.stdout
+
+
+def test_reference_model_handle_matches_per_call_pipeline(reference):
+    """bench.py --impl reference times pipeline_dc on a reference layer / predictor built once;
+    it must be bit-identical to the per-call path (with and without a mask override)."""
+    g = reference.generate(42, 256, 1024, 32)
+    h = reference.model(g)
+    try:
+        for mo in (None, (np.arange(1024) % 3 == 0).astype(np.uint8)):
+            a = reference.model_pipeline_dc(h, g["x"], 256, mo)
+            b = reference.pipeline_dc(g, g["x"], mo)
+            assert np.array_equal(a["y"].view(np.uint32), b["y"].view(np.uint32)) and a["alive"] == b["alive"]
+    finally:
+        reference.model_free(h)

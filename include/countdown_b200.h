@@ -174,7 +174,11 @@ CD_API int cd_predict_logits(cd_layer* h, int64_t batch, const float* x, float* 
  * method CD_METHOD_DENSE ignores tau.  Optional outputs (NULL to skip):
  *   d_mask: batch x d_inter uint8, d_indicator: batch x d_inter f32 (u for MC, logits for
  *   DC), d_alive: batch int32 per-sample alive counts.
- * d_mask_override (DC only, NULL for the thresholded path): batch x d_inter uint8. */
+ * d_mask_override (DC only, NULL for the thresholded path): batch x d_inter uint8.
+ * The step kernels are persistent (one CTA per SM, all resident at once): calls must not
+ * execute concurrently with another handle's call on a different stream of the same device
+ * (order them on one stream, or join the streams).  The host-buffer entry points use one
+ * internal stream per device and are safe from any thread. */
 CD_API int cd_forward_device(cd_layer* h, int method, int64_t batch, const float* d_x, float tau,
                       int reduction, const uint8_t* d_mask_override, float* d_y,
                       uint8_t* d_mask, float* d_indicator, int32_t* d_alive, void* stream);

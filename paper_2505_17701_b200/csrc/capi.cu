@@ -151,10 +151,9 @@ struct cd_layer {
         return static_cast<T*>(p);
     }
     ~cd_layer() {
-        if (stream) {
+        if (stream) {  // the device's shared stream: drained, not destroyed
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
-            cudaStreamDestroy(stream);
         }
         if (blas) cublasDestroy(blas);
         if (hg.exec) cudaGraphExecDestroy(hg.exec);
@@ -584,6 +583,22 @@ void check_finite_blob(const float* p, size_t n, const std::string& path, const 
                                   std::to_string(i));
 }
 
+// One internal stream per device, shared by every handle on it.  The persistent kernels
+// (k_dc_fused, k_mc_fused, k_tc_fused) need all of their CTAs resident at once; two of them
+// running concurrently on different streams could each hold part of the GPU and wait forever
+// for the rest.  Sharing the stream serialises the host-buffer calls of all handles.
+cudaStream_t device_stream(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = streams.find(device);
+    if (it != streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    streams.emplace(device, s);
+    return s;
+}
+
 cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_t re, int act,
                       int dtype, const float* w_up, const float* w_gate, const float* w_down,
                       bool predictor_only = false) {
@@ -607,7 +622,7 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     auto h = std::make_unique<cd_layer>();
     h->device = device;
     h->num_sms = prop.multiProcessorCount;
-    ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    h->stream = device_stream(device);
     cdk::LayerDev& L = h->L;
     L.d = d;
     L.F = re - rb;

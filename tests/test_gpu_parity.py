@@ -441,3 +441,34 @@ def test_host_call_graph_replay_and_recapture(oracle):
             yd = cd.exec_dense(layer, X, FAST)
             for b in range(2):
                 assert rel_l2(yd[b], oracle.forward_dense(g, X[b])["y"]) <= 1e-4
+
+
+@pytest.mark.timeout(300)
+def test_concurrent_host_calls_on_two_handles(oracle):
+    """Host-buffer calls on two handles from two threads at once (ctypes drops the GIL): the
+    persistent step kernels need the whole GPU, so all handles share one device stream and the
+    calls serialise instead of deadlocking; every result matches the single-threaded one."""
+    import threading
+    cases = [make_case(oracle, 106 + k, 512, 2048, 64, 0, "bf16") for k in range(2)]
+    want = []
+    for g, layer, pred in cases:
+        want.append(cd.pipeline_dc(layer, g["x"], pred, FAST, tau_d=0.0).y.copy())
+    errors = []
+
+    def worker(k):
+        g, layer, pred = cases[k]
+        try:
+            for _ in range(60):
+                got = cd.pipeline_dc(layer, g["x"], pred, FAST, tau_d=0.0).y
+                if rel_l2(got, want[k]) > 1e-5:
+                    errors.append((k, rel_l2(got, want[k])))
+        except Exception as e:  # noqa: BLE001
+            errors.append((k, repr(e)))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(240)
+    assert not any(t.is_alive() for t in ts), "host calls did not finish"
+    assert not errors, errors

@@ -500,10 +500,14 @@ cudaError_t launch_mc_fused(const LayerDev& L, const Scratch& S, const float* x,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
                 p.use_map = 1;
         }
-        static unsigned long long* tl_env = [] {
-            const char* e = std::getenv("CD_MC_TL");
-            return e ? reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 10)) : nullptr;
-        }();
+        static unsigned long long* tl_env = []() -> unsigned long long* {
+#ifdef CD_TIMELINE  // development builds only: a device address taken from the environment
+        const char* e = std::getenv("CD_MC_TL");
+        return e ? reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 10)) : nullptr;
+#else
+        return nullptr;
+#endif
+    }();
         p.tl = tl_env;
         return launch_ex(kern, dim3(G), dim3(threads), smem, c, true, p);
     };

@@ -695,9 +695,13 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
         const char* e = std::getenv("CD_TC_GRID");
         return e ? std::atoi(e) : 0;
     }();
-    static unsigned long long* tl_env = [] {
-        const char* e = std::getenv("CD_TC_TL");  // development: device buffer for phase stamps
+    static unsigned long long* tl_env = []() -> unsigned long long* {
+#ifdef CD_TIMELINE  // development builds only: a device address taken from the environment
+        const char* e = std::getenv("CD_TC_TL");
         return e ? reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 10)) : nullptr;
+#else
+        return nullptr;
+#endif
     }();
     a.tl = tl_env;
     int grid = static_cast<int>(std::min<int64_t>(std::min(c.num_sms, kMaxCtas), units));

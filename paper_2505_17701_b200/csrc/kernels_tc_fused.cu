@@ -663,9 +663,13 @@ cudaError_t launch_batched_fused(const LayerDev& L, const Plan& p, void* ws_base
     a.lat32 = lat32;
     a.latb = latb;
     a.ldr = ldr;
-    static unsigned long long* tl_env = [] {
+    static unsigned long long* tl_env = []() -> unsigned long long* {
+#ifdef CD_TIMELINE  // development builds only: a device address taken from the environment
         const char* e = std::getenv("CD_TC_TL");
         return e ? reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 10)) : nullptr;
+#else
+        return nullptr;
+#endif
     }();
     a.tl = tl_env;
     static const int pf_env = [] {

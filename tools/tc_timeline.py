@@ -8,6 +8,7 @@ import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ.setdefault("CD_LIB_DIR", "_lib_tl")  # the phase-stamp hooks exist only in the timeline build
 sys.path.insert(0, ROOT)
 tl = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
 os.environ["CD_TC_TL"] = str(tl.data_ptr())

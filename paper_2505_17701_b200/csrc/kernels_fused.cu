@@ -270,15 +270,16 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
                 xr[b][j][4] = hi.x; xr[b][j][5] = hi.y; xr[b][j][6] = hi.z; xr[b][j][7] = hi.w;
             }
         }
+        unsigned prev_actives = 0;  // thread 0: the previous launch's active count (in flight)
         if (threadIdx.x == 0) {
             TL(5, 1);
             const uint32_t t = static_cast<uint32_t>(__ldcg(S.ctl + kCtlEpoch)) + 1u;
             cnt[NB + 1] = static_cast<int>(t);
             // own-work cap: the previous launch's active count spread over the grid (the first
-            // launch keeps everything); queue counters of the NEXT launch are reset here (the
-            // launch that used them last has completed)
-            const unsigned prev = __ldcg(S.ctl + kCtlQueue + ((t + 2u) % 3u) * 32u + 3);
-            cnt[NB + 2] = prev > 0 ? static_cast<int>((prev + G - 1) / G) : (1 << 30);
+            // launch keeps everything).  Only requested here -- it is consumed at the end of
+            // stage 2, so stage 1 waits for one round trip (the tag), not two.  Queue counters of
+            // the NEXT launch are reset here (the launch that used them last has completed).
+            prev_actives = __ldcg(S.ctl + kCtlQueue + ((t + 2u) % 3u) * 32u + 3);
             if (blockIdx.x == 0) {
                 unsigned* nq = S.ctl + kCtlQueue + ((t + 1u) % 3u) * 32u;
                 nq[0] = 0u; nq[1] = 0u; nq[2] = 0u; nq[3] = 0u;
@@ -529,6 +530,7 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
         }
         if (threadIdx.x == 0) {
             TL(6, 1);
+            cnt[NB + 2] = prev_actives > 0 ? static_cast<int>((prev_actives + G - 1) / G) : (1 << 30);
         }
         named_bar_sync(kBarC, nc);
         if (threadIdx.x == 0) TL(5, 4);

@@ -212,11 +212,26 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
         const int ct = threadIdx.x;
         const int nvec = static_cast<int>(L.ld / kVec);
         pdl_wait();
+        // x into registers first: in flight together with thread 0's launch-tag read
+        float xr[VPT][8];
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int vec = ct + j * nc;
+            float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+            const int64_t col = (int64_t)vec * kVec;
+            if (vec < nvec) {
+                const float4* src = reinterpret_cast<const float4*>(P.x + col);
+                if (col < L.d) lo = __ldcg(src);
+                if (col + 4 < L.d) hi = __ldcg(src + 1);
+            }
+            xr[j][0] = lo.x; xr[j][1] = lo.y; xr[j][2] = lo.z; xr[j][3] = lo.w;
+            xr[j][4] = hi.x; xr[j][5] = hi.y; xr[j][6] = hi.z; xr[j][7] = hi.w;
+        }
+        unsigned prev_actives = 0;  // thread 0: consumed after stage 1 (one round trip here, not two)
         if (threadIdx.x == 0) {
             const uint32_t t = static_cast<uint32_t>(__ldcg(S.ctl + kCtlEpoch)) + 1u;
             cnt[1] = static_cast<int>(t);
-            const unsigned prev = __ldcg(S.ctl + kCtlQueue + ((t + 2u) % 3u) * 32u + 3);
-            cnt[2] = prev > 0 ? static_cast<int>((prev + G - 1) / G) : (1 << 30);
+            prev_actives = __ldcg(S.ctl + kCtlQueue + ((t + 2u) % 3u) * 32u + 3);
             if (blockIdx.x == 0) {
                 unsigned* nq = S.ctl + kCtlQueue + ((t + 1u) % 3u) * 32u;
                 nq[0] = 0u; nq[1] = 0u; nq[2] = 0u; nq[3] = 0u;
@@ -232,20 +247,6 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
         }
         named_bar_sync(kBarC, nc);
         const uint32_t tag = static_cast<uint32_t>(cnt[1]);
-        float xr[VPT][8];
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            const int vec = ct + j * nc;
-            float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
-            const int64_t col = (int64_t)vec * kVec;
-            if (vec < nvec) {
-                const float4* src = reinterpret_cast<const float4*>(P.x + col);
-                if (col < L.d) lo = __ldcg(src);
-                if (col + 4 < L.d) hi = __ldcg(src + 1);
-            }
-            xr[j][0] = lo.x; xr[j][1] = lo.y; xr[j][2] = lo.z; xr[j][3] = lo.w;
-            xr[j][4] = hi.x; xr[j][5] = hi.y; xr[j][6] = hi.z; xr[j][7] = hi.w;
-        }
 
         // ---------------------------------------------------------- stage 1: u = W_up x, threshold
         // Stages are consumed (and handed back to the producer) one by one, but reduced across
@@ -317,6 +318,8 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
                 }
             }
         }
+        if (threadIdx.x == 0)  // own-work cap: the previous launch's active count over the grid
+            cnt[2] = prev_actives > 0 ? static_cast<int>((prev_actives + G - 1) / G) : (1 << 30);
         named_bar_sync(kBarC, nc);
         if (threadIdx.x == 0) mstamp(P, 2);
         named_bar_arrive(kBarK, nc + kWarp);  // producer may schedule stage 3 now

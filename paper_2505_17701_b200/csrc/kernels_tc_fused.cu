@@ -75,8 +75,10 @@ __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned v) {
     }
 }
 
+constexpr int kThreadsF = kThreads + 32;  // + one latent helper warp
+
 template <int KIND, int ACT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsF, 1)
 k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUtensorMap m_gate,
            const __grid_constant__ CUtensorMap m_x, const __grid_constant__ CUtensorMap m_tb,
            const __grid_constant__ CUtensorMap m_lat, const __grid_constant__ CUtensorMap m_ta,
@@ -309,7 +311,7 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
                 umma_commit(tfull);
             }
         }
-    } else {
+    } else if (warp < 2 + kEpiWarps) {
         // ================= epilogue warps
         const int g = warp & 3;
         const int half = (warp - 2) >> 2;
@@ -349,29 +351,11 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
                 }
                 done_seg();
             }
-            // all latent partials in: every CTA re-splits its slice into bf16 pairs (pair layout,
-            // TMA-read by the predictor blocks), then counts itself into kWLatReady
+            // this CTA's latent partials are in: count it (the helper warp re-splits once every
+            // CTA has counted -- the epilogue goes straight on to phase A and keeps TMEM moving)
             __threadfence();
             named_bar_sync(1, kEpiThreads);
-            if (et == 0) {
-                atomicAdd(a.flags + kWLatCount, 1u);
-                spin_until_geq(a.flags + kWLatCount, static_cast<unsigned>(G));
-                __threadfence();
-            }
-            named_bar_sync(1, kEpiThreads);
-            const int64_t n = static_cast<int64_t>(a.nb) * a.r;
-            for (int64_t e = c * n / G + et; e < (c + 1) * n / G; e += kEpiThreads) {
-                const int64_t b = e / a.r, jr = e - b * a.r;
-                const float v = __ldcg(a.lat32 + b * a.ldr + jr);
-                const int64_t row = (b / nbt) * N + b % nbt;
-                const __nv_bfloat16 h = __float2bfloat16_rn(v);
-                a.latb[row * a.ldr + jr] = h;
-                a.latb[(row + nbt) * a.ldr + jr] = __float2bfloat16_rn(v - __bfloat162float(h));
-            }
-            fence_proxy_async_global();
-            __threadfence();
-            named_bar_sync(1, kEpiThreads);
-            if (et == 0) atomicAdd(a.flags + kWLatReady, 1u);
+            if (et == 0) atomicAdd(a.flags + kWLatCount, 1u);
         }
         // ---- phase A: gate/up tiles (contributors park partials, finishers apply the masks)
         for (int si = 0; seg_at(c, si, UA, G, nkbA, sg); ++si) {
@@ -555,16 +539,35 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
         }
         named_bar_sync(1, kEpiThreads);
         if (et == 0) fstamp(a, 5);
-        if (et == 0 && atomicAdd(a.flags + kWEndCount, 1u) == static_cast<unsigned>(G - 1)) {
-            // every CTA is past all its waits: reset the control words for the next launch
-            a.flags[kWLatCount] = 0u;
-            a.flags[kWLatReady] = 0u;
-            a.flags[kWSCount] = 0u;
-            a.flags[kWEndCount] = 0u;
-        }
         tc_fence_before();
+    } else if (kZ) {
+        // ================= latent helper warp: once every CTA's phase-0 partials are in, re-split
+        // this CTA's slice of the f32 latent into the bf16 pairs the predictor blocks read
+        if (lane == 0) spin_until_geq(a.flags + kWLatCount, static_cast<unsigned>(G));
+        __syncwarp();
+        __threadfence();
+        const int64_t n = static_cast<int64_t>(a.nb) * a.r;
+        for (int64_t e = c * n / G + lane; e < (c + 1) * n / G; e += 32) {
+            const int64_t b = e / a.r, jr = e - b * a.r;
+            const float v = __ldcg(a.lat32 + b * a.ldr + jr);
+            const int64_t row = (b / nbt) * N + b % nbt;
+            const __nv_bfloat16 h = __float2bfloat16_rn(v);
+            a.latb[row * a.ldr + jr] = h;
+            a.latb[(row + nbt) * a.ldr + jr] = __float2bfloat16_rn(v - __bfloat162float(h));
+        }
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(a.flags + kWLatReady, 1u);
     }
     __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(a.flags + kWEndCount, 1u) == static_cast<unsigned>(G - 1)) {
+        // every warp of every CTA is past all its waits: reset the control words for the next launch
+        a.flags[kWLatCount] = 0u;
+        a.flags[kWLatReady] = 0u;
+        a.flags[kWSCount] = 0u;
+        a.flags[kWEndCount] = 0u;
+    }
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
@@ -697,7 +700,7 @@ cudaError_t launch_batched_fused(const LayerDev& L, const Plan& p, void* ws_base
 #undef CD_TCF_PICK
     if (!fn) return cudaErrorInvalidValue;
     if ((e = set_smem(fn, smem)) != cudaSuccess) return e;
-    fn<<<G, kThreads, smem, c.stream>>>(m_up, m_gate, m_x, m_tb, m_lat, m_ta, m_w, m_s, a);
+    fn<<<G, kThreadsF, smem, c.stream>>>(m_up, m_gate, m_x, m_tb, m_lat, m_ta, m_w, m_s, a);
     return cudaGetLastError();
 }
 

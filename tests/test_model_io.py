@@ -94,3 +94,24 @@ def test_device_loader_matches_host_arrays(reference, oracle, tmp_path):
     open(bad, "wb").write(b"XDWN1" + open(path, "rb").read()[5:])
     with pytest.raises(DataError, match="bad magic"):
         cd.DeviceLayer.load(str(bad))
+
+
+@pytest.mark.gpu
+def test_device_loader_bf16_batched_tensor_cores(reference, oracle, tmp_path):
+    """A CDWN1 file loaded straight to bf16 device weights serves a batch of 16 on the
+    tensor-core path; each sample matches the oracle on the bf16-rounded weights (1e-4)."""
+    from conftest import bf16_round, rel_l2
+    path = tmp_path / "m.cdwn"
+    reference.write_model(path, 107, 384, 1536, 48, 1, 0.9)
+    dev = cd.DeviceLayer.load(str(path), "bf16")
+    g = oracle.generate(107, 384, 1536, 48)
+    g = {k: bf16_round(v) for k, v in g.items()}
+    rng = oracle.rng(5)
+    X = np.stack([rng.normals_f(384) for _ in range(16)])
+    y, mask, alive, z = dev.pipeline_dc(X, 0.05, cd.Reduction.UnorderedAccumulate, None, True)
+    assert dev.last_path() == "tensor"
+    for b in range(16):
+        _, zb = oracle.lowrank_logits(g["theta_a"], g["theta_b"], X[b])
+        assert rel_l2(z[b], zb) <= 1e-5
+        assert rel_l2(y[b], oracle.forward_sparse(g, X[b], mask[b], act=1)) <= 1e-4
+        assert alive[b] == int(mask[b].sum())

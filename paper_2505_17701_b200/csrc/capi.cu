@@ -198,14 +198,17 @@ struct Req {
 
 constexpr int kTcMinBatch = 8;  // batches from here on run on the tensor cores (bf16 layers)
 
-// The tensor-core path (kernels_tc.cu) covers bf16 layers at batch >= 8: pipelines, dense, and
-// exec_dc (its masks act as the override); exec_mc / exec_cats with caller-given u stay on the
-// CUDA-core chain.
+// The tensor-core path (kernels_tc.cu) covers bf16 layers at batch >= 8 for the calls that
+// threshold their own masks (pipelines, dense).  Caller-supplied masks -- exec_dc / exec_mc /
+// exec_cats and pipeline_dc's mask_override -- stay on the CUDA-core kernels at every batch
+// size: the reference guarantees a dead lane's rows and u entries are never read (its tests
+// poison them with NaN, test_blocked_exec.cpp:101-116), while the row-union GEMM reads every
+// row and 0 x NaN would reach y.
 bool tc_eligible(const cd_layer* h, const Req& r) {
     if (!h->use_tc || h->L.dtype != CD_DTYPE_BF16 || !h->L.w_up || r.nb < kTcMinBatch || r.marks) return false;
     if (r.reduction != CD_REDUCTION_UNORDERED) return false;
-    if (r.with_masks) return r.method == cdk::kDC;
-    return r.method != cdk::kDC || r.ovr || h->L.theta_bt;
+    if (r.with_masks || r.ovr) return false;
+    return r.method != cdk::kDC || h->L.theta_bt;
 }
 
 cublasHandle_t blas_of(cd_layer* h) {

@@ -1,6 +1,8 @@
 """Batched decode (B >= 8) and dense prefill on the tcgen05 tensor cores (SURVEY.md section 8f
 row 1, BASELINE.json config 5) against the CPU oracle.
 
+Caller-supplied masks (exec_*, mask_override) stay on the CUDA-core kernels at every batch size
+(dead lanes are never read); the tensor-core path serves the thresholding calls.
 The reference semantics are per sample (blocked_exec.cpp:252-298 / :350-379; main.cpp:239-282):
 each sample's y must equal the oracle's forward_sparse on that sample's own mask.  Decode runs
 activations as bf16 (hi, lo) pairs, so the contract is the fast path's: y within 1e-4 relative
@@ -100,25 +102,40 @@ def test_tc_cats_pipeline(oracle, B):
 
 
 @pytest.mark.parametrize("B", [8, 64, 65])
-def test_tc_exec_dc_masks_and_override(oracle, B):
-    """exec_dc with caller masks and pipeline_dc(mask_override) at batch >= 8 (per-sample masks,
-    including all-dead and all-live rows)."""
+def test_batched_caller_masks_never_read_dead_lanes(oracle, B):
+    """exec_dc / exec_mc / pipeline_dc(mask_override) at batch >= 8 on a bf16 layer: the rows
+    and u entries of lanes dead in EVERY sample are NaN-poisoned (test_blocked_exec.cpp:101-116
+    at batch scale) and must not reach y.  Caller-supplied masks therefore stay on the CUDA-core
+    kernels (the row-union GEMM would read them); per-sample masks include all-dead and
+    all-live rows."""
     seed, d, F, r = 203, 130, 500, 24
-    g, layer, pred = make(oracle, seed, d, F, r)
+    g, layer_ok, pred = make(oracle, seed, d, F, r)
     X = batch(oracle, 5, B, d)
     rng = np.random.default_rng(B)
     masks = (rng.random((B, F)) < 0.3).astype(np.uint8)
+    masks[:, :50] = 0        # dead in every sample: poisoned below
     masks[0] = 0
-    masks[1] = 1
+    masks[1, 50:] = 1
+    want = [oracle.forward_sparse(g, X[b], masks[b]) for b in range(B)]
+    bad = {k: v.copy() for k, v in g.items()}
+    for k in ("w_up", "w_gate", "w_down"):
+        bad[k][:50] = np.nan
+    layer = cd.GatedMlpLayer(d, F, 0, bad["w_up"], bad["w_gate"], bad["w_down"], device_dtype="bf16")
     y = cd.exec_dc(layer, X, masks, FAST)
-    assert layer.device_layer().last_path() == "tensor"
-    assert np.all(y[0] == 0)
+    assert layer.device_layer().last_path() == "fast"
+    assert np.all(np.isfinite(y)) and np.all(y[0] == 0)
+    U = np.stack([oracle.gemv(g["w_up"], X[b]) for b in range(B)])
+    U[:, :50] = np.nan
+    y_mc = cd.exec_mc(layer, X, U, masks, FAST)
+    assert np.all(np.isfinite(y_mc))
     for b in range(B):
-        assert rel_l2(y[b], oracle.forward_sparse(g, X[b], masks[b])) <= 1e-4
-    res = cd.pipeline_dc(layer, X, pred, FAST, mask_override=masks)
+        assert rel_l2(y[b], want[b]) <= 1e-4
+        assert rel_l2(y_mc[b], want[b]) <= 1e-4
+    res = cd.pipeline_dc(layer_ok, X, pred, FAST, mask_override=masks)
+    assert layer_ok.device_layer(pred).last_path() == "fast"
     for b in range(B):
         assert np.array_equal(res.mask[b].alive, masks[b])
-        assert rel_l2(res.y[b], y[b]) <= 1e-5
+        assert rel_l2(res.y[b], want[b]) <= 1e-4
 
 
 @pytest.mark.parametrize("B", [8, 64, 300])

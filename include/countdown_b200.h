@@ -27,8 +27,10 @@
  *                                 y within 1e-4 relative L2 of ORDERED in f32
  *                                 (test_blocked_exec.cpp:87-99).
  *     blk_m / blk_n have no GPU meaning; results are invariant to them (acceptance.cpp:336-342).
- *   - Thread safety: every call on a handle is serialised by a per-handle mutex; distinct
- *     handles are independent.  No host threads are spawned.
+ *   - Thread safety: every entry point may be called from any thread.  Calls that enqueue
+ *     work on a device's internal stream (host-buffer operators, create / load / destroy,
+ *     set_predictor) are serialised by a per-device lock, then a per-handle lock.  No host
+ *     threads are spawned.
  */
 #ifndef COUNTDOWN_B200_H
 #define COUNTDOWN_B200_H
@@ -99,7 +101,8 @@ CD_API int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* thet
 /* read_model (model_io.cpp:140-224) straight to the device: parses and validates a CDWN1 model
  * file exactly as the reference does (magic, header schema, byte counts, finite values ->
  * CD_ERR_DATA with the reference's messages), uploads the layer in `dtype` and attaches a
- * low-rank predictor.  dims_out[5] (optional) = {d_model, d_inter, d_rank, activation, seed};
+ * low-rank predictor.  dims_out[5] (optional) = {d_model, d_inter, d_rank, activation, seed}
+ * (seed: the header's uint64 bit pattern, read exactly as get<uint64_t>, model_io.cpp:153);
  * d_rank is 0 without a predictor and -1 for a ternary predictor (not attached: the B200 path
  * runs the low-rank predictor only). */
 CD_API int cd_layer_load_cdwn1(int device, const char* path, int dtype, cd_layer** out, int64_t* dims_out);
@@ -122,6 +125,18 @@ CD_API int cd_layer_last_launches(const cd_layer* h, int* launches);
 #define CD_PATH_FAST 1
 #define CD_PATH_TENSOR 2
 CD_API int cd_layer_last_path(const cd_layer* h, int* path);
+
+/* Engine selection (no reference equivalent: the reference has one CPU engine).  Default:
+ * all on.  CD_ENGINE_FUSED: batch <= 4 D-/M-CountDown steps as one persistent kernel (off:
+ * the multi-kernel chains).  CD_ENGINE_TENSOR: bf16 layers at batch >= 8 on the tcgen05
+ * masked row-union GEMM (off: the CUDA-core kernels in chunks of 4).  CD_ENGINE_HOST_GRAPH:
+ * host-buffer calls replay a captured CUDA graph of their whole sequence.  Results stay
+ * within each reduction mode's contract whatever the selection; this is for A/B tests. */
+#define CD_ENGINE_FUSED 1
+#define CD_ENGINE_TENSOR 2
+#define CD_ENGINE_HOST_GRAPH 4
+#define CD_ENGINE_ALL 7
+CD_API int cd_layer_set_engines(cd_layer* h, int engines);
 
 /* ---------------------------------------------------------------- host-buffer operators
  * Synchronous: inputs are read from host memory, outputs written to host memory before

@@ -20,6 +20,7 @@ ACT_SILU, ACT_GELU_TANH = 0, 1
 DTYPE_F32, DTYPE_BF16 = 0, 1
 REDUCTION_ORDERED, REDUCTION_UNORDERED = 0, 1
 METHOD_DENSE, METHOD_MC, METHOD_DC, METHOD_CATS = 0, 1, 2, 3
+ENGINE_FUSED, ENGINE_TENSOR, ENGINE_HOST_GRAPH, ENGINE_ALL = 1, 2, 4, 7
 
 
 class DataError(RuntimeError):
@@ -64,6 +65,7 @@ _SIGNATURES = {
     "cd_predict_logits": [_vp, _i64, _vp, _vp],
     "cd_forward_device": [_vp, _i32, _i64, _vp, _f32, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "cd_layer_sync": [_vp],
+    "cd_layer_set_engines": [_vp, _i32],
     "cd_predictor_create": [_i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp],
     "cd_bench_device": [_vp, _i32, _i64, _vp, _f32, _i32, _i64, _i64, _vp],
     "cd_bench_stages": [_vp, _i32, _i32, _i64, _vp, _f32, _i64, _i64, _vp, _vp],

@@ -245,7 +245,7 @@ class DeviceLayer:
                                         ptr(dims)))
         dl = DeviceLayer(out, int(dims[0]), int(dims[1]), max(0, int(dims[2])))
         dl.activation = Activation(int(dims[3]))
-        dl.seed = int(dims[4])
+        dl.seed = int(dims[4]) & 0xFFFFFFFFFFFFFFFF  # the header's uint64 bit pattern
         dl.predictor_kind = "lowrank" if dims[2] > 0 else ("ternary" if dims[2] < 0 else None)
         return dl
 
@@ -376,6 +376,13 @@ class DeviceLayer:
 
     def sync(self) -> None:
         check(lib().cd_layer_sync(self.raw))
+
+    def set_engines(self, fused: bool = True, tensor: bool = True, host_graph: bool = True) -> None:
+        """cd_layer_set_engines: pick the engines this handle may use (A/B tests; all on by
+        default).  Results stay within each reduction mode's contract whatever the choice."""
+        flags = ((_capi.ENGINE_FUSED if fused else 0) | (_capi.ENGINE_TENSOR if tensor else 0) |
+                 (_capi.ENGINE_HOST_GRAPH if host_graph else 0))
+        check(lib().cd_layer_set_engines(self.raw, flags))
 
     @staticmethod
     def bench_stages(layers: "list[DeviceLayer]", method: int, x_dev, tau: float, warmup: int,

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cerrno>
 #include <cmath>
 #include <fstream>
 #include <map>
@@ -59,6 +60,7 @@ struct Grow {
     bool host = false;
     void* p = nullptr;
     size_t cap = 0;
+    uint64_t* gen = nullptr;  // owner's generation: bumped when the buffer moves
     Grow() = default;
     explicit Grow(bool on_host) : host(on_host) {}
     Grow(const Grow&) = delete;
@@ -70,6 +72,7 @@ struct Grow {
             const size_t want = std::max(bytes, cap * 2);
             ck(host ? cudaMallocHost(&p, want) : cudaMalloc(&p, want), host ? "cudaMallocHost" : "cudaMalloc");
             cap = want;
+            if (gen) ++*gen;
         }
         return static_cast<T*>(p);
     }
@@ -90,14 +93,20 @@ struct cd_layer {
     cdk::Scratch S;
     int64_t F_total = 0, row_begin = 0;
     cudaStream_t stream = nullptr;
+    std::recursive_mutex* dev_mu = nullptr;  // the device's lock (see device_stream)
     std::mutex mu;
-    std::vector<void*> dev_allocs;
+    // Device-state generation: bumped whenever a pointer a captured host graph could hold
+    // changes (predictor re-attached, a workspace regrown).  Part of the host-graph key.
+    uint64_t gen = 1;
+    std::vector<std::pair<void*, size_t>> dev_allocs;
     std::vector<void*> host_allocs;
     int64_t bytes = 0;
     int last_launches = 0;
     int last_path = CD_PATH_FAST;
-    bool use_fused = true;  // D-CountDown as one persistent kernel (CD_DC_CHAIN=1 forces the chain)
-    bool use_tc = true;     // batches >= kTcMinBatch of a bf16 layer on the tensor cores (CD_TC=0: off)
+    // engines (cd_layer_set_engines): all on by default
+    bool use_fused = true;  // batch <= 4 DC / MC as one persistent kernel (off: the kernel chains)
+    bool use_tc = true;     // batches >= kTcMinBatch of a bf16 layer on the tensor cores
+    bool weights_finite = true;  // every uploaded weight finite: the row-union GEMM may read any row
     cublasHandle_t blas = nullptr;
     Grow tc_ws, blas_ws;    // tensor-core path workspace; cuBLAS workspace (graph-capture safe)
     // host-call CUDA graph: [H2D inputs, kernels, D2H outputs] replayed while the call signature
@@ -108,12 +117,11 @@ struct cd_layer {
         cudaGraphExec_t exec = nullptr;
         int launches = 0, path = 0;
     } hg;
-    bool use_host_graph = true;  // CD_HOST_GRAPH=0 disables
+    bool use_host_graph = true;  // host-buffer calls replay a captured graph
     bool mapped_staging = true;  // fixed pinned staging is device-addressable (copy kernels)
     // large-batch staging (host-buffer calls on the tensor-core path)
     Grow g_dx, g_dy, g_dmask_in, g_dmask_out, g_du_in, g_dind, g_dalive;
     Grow g_hx{true}, g_hy{true}, g_hmask{true}, g_hind{true}, g_halive{true};
-    int keep0 = 0;          // fused kernel: own active neurons streamed before rebalancing (CD_KEEP0)
     // device staging for the host-buffer entry points
     float* d_x = nullptr;
     float* d_y = nullptr;
@@ -132,10 +140,20 @@ struct cd_layer {
     template <typename T> T* dalloc(size_t n, bool zero = true) {
         void* p = nullptr;
         ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
-        dev_allocs.push_back(p);
+        dev_allocs.emplace_back(p, n * sizeof(T));
         bytes += static_cast<int64_t>(n * sizeof(T));
         if (zero) ck(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)), "cudaMemset");
         return static_cast<T*>(p);
+    }
+    // Free one dalloc'd buffer (a replaced predictor) once the stream no longer uses it.
+    void dfree(const void* p) {
+        for (auto it = dev_allocs.begin(); it != dev_allocs.end(); ++it)
+            if (it->first == p) {
+                bytes -= static_cast<int64_t>(it->second);
+                cudaFree(it->first);
+                dev_allocs.erase(it);
+                return;
+            }
     }
     template <typename T> T* halloc(size_t n) {
         void* p = nullptr;
@@ -157,7 +175,7 @@ struct cd_layer {
         }
         if (blas) cublasDestroy(blas);
         if (hg.exec) cudaGraphExecDestroy(hg.exec);
-        for (void* p : dev_allocs) cudaFree(p);
+        for (auto& a : dev_allocs) cudaFree(a.first);
         for (void* p : host_allocs) cudaFreeHost(p);
     }
 };
@@ -167,13 +185,48 @@ namespace {
 using cdk::kMaxBatch;
 using cdk::kMaxBatchFast;
 
+// One internal stream and one lock per device, shared by every handle on it.
+//  - The persistent kernels (k_dc_fused, k_mc_fused, k_tc_fused) need all of their CTAs
+//    resident at once; two of them running concurrently on different streams could each hold
+//    part of the GPU and wait forever for the rest.  Sharing the stream serialises them.
+//  - The lock is held across every call that enqueues on that stream (host-buffer operators,
+//    uploads, predictor attach, destroy).  A host call captures its sequence into a CUDA graph
+//    on the shared stream; without the lock, another thread's work enqueued meanwhile would
+//    become part of that graph.
+struct DeviceCtx {
+    cudaStream_t stream = nullptr;
+    std::recursive_mutex mu;
+};
+
+DeviceCtx& device_ctx(int device) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<DeviceCtx>> ctxs;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = ctxs.find(device);
+    if (it != ctxs.end()) return *it->second;
+    auto c = std::make_unique<DeviceCtx>();
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    DeviceCtx& ref = *c;
+    ctxs.emplace(device, std::move(c));
+    return ref;
+}
+
+// Device lock, then handle lock (always in this order).
+struct CallLock {
+    std::unique_lock<std::recursive_mutex> d;
+    std::unique_lock<std::mutex> h;
+    explicit CallLock(cd_layer* l) : d(*l->dev_mu), h(l->mu) {}
+};
+
+
 // Upload rows [row_begin, row_end) of a full host matrix (rows x cols f32) into a padded
 // device matrix (dtype, row stride ld), via an f32 staging buffer and the pack kernel.
 void upload_rows(cd_layer* h, const float* host, int64_t row_begin, int64_t nrows, int64_t cols,
-                 void* dst, int64_t ld_pad, int64_t ld_dst, float* tmp) {
+                 void* dst, int64_t ld_pad, int64_t ld_dst, float* tmp, int* nonfinite = nullptr) {
     ck(cudaMemcpyAsync(tmp, host + row_begin * cols, sizeof(float) * nrows * cols,
                        cudaMemcpyHostToDevice, h->stream),
        "upload");
+    if (nonfinite) ck(cdk::launch_count_nonfinite(tmp, nrows * cols, nonfinite, h->stream), "upload check");
     ck(cdk::launch_pack_rows(tmp, nrows, cols, cols, dst, h->L.dtype, ld_pad, ld_dst, h->stream), "pack_rows");
 }
 
@@ -206,6 +259,7 @@ constexpr int kTcMinBatch = 8;  // batches from here on run on the tensor cores 
 // row and 0 x NaN would reach y.
 bool tc_eligible(const cd_layer* h, const Req& r) {
     if (!h->use_tc || h->L.dtype != CD_DTYPE_BF16 || !h->L.w_up || r.nb < kTcMinBatch || r.marks) return false;
+    if (!h->weights_finite) return false;
     if (r.reduction != CD_REDUCTION_UNORDERED) return false;
     if (r.with_masks || r.ovr) return false;
     return r.method != cdk::kDC || h->L.theta_bt;
@@ -288,7 +342,7 @@ int run_chain(cd_layer* h, const Req& r) {
                 launches += 2;
             } else if (h->use_fused &&
                        cdk::launch_dc_fused(L, S, xc, n, r.tau, r.ovr ? r.ovr + c0 * F : nullptr, yc, mo, io, ao,
-                                            c, h->keep0) == cudaSuccess) {
+                                            c) == cudaSuccess) {
                 launches += 1;
                 mark(0);
             } else {
@@ -384,7 +438,7 @@ struct HostIO {
 };
 
 void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
-    std::lock_guard<std::mutex> g(h->mu);
+    CallLock lk(h);
     ck(cudaSetDevice(h->device), "cudaSetDevice");
     const int64_t d = h->L.d, F = h->L.F;
     cudaStream_t s = h->stream;
@@ -418,6 +472,7 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
               (static_cast<uint64_t>(base.method) << 16) ^ (static_cast<uint64_t>(base.reduction) << 12) ^
               (base.with_masks ? 1u << 8 : 0u) ^ (io.ovr ? 1u << 9 : 0u) ^ (io.masks_in ? 1u << 10 : 0u) ^
               (io.u_in ? 1u << 11 : 0u) ^ (io.mask_out ? 1u << 5 : 0u) ^ (io.ind_out ? 1u << 6 : 0u) ^ 1u;
+        key = key * 0x9E3779B97F4A7C15ull ^ h->gen;  // device state the graph's pointers come from
         if (h->hg.key != key) {
             if (h->hg.exec) cudaGraphExecDestroy(h->hg.exec);
             h->hg = {};
@@ -432,6 +487,7 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
         if (io.u_in) std::memcpy(h_ind, io.u_in + c0 * F, sizeof(float) * n * F);
         const bool replay = graphable && h->hg.exec;
         const bool capture = graphable && !replay && ++h->hg.seen >= 2;
+        const uint64_t gen_before = h->gen;
         if (replay) {
             ck(cudaGraphLaunch(h->hg.exec, s), "graph launch");
             launches += h->hg.launches;
@@ -489,6 +545,11 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
             h->hg.launches = nl;
             h->hg.path = h->last_path;
             ck(cudaGraphLaunch(h->hg.exec, s), "graph launch");
+            if (h->gen != gen_before) {  // a buffer moved while capturing: never replay this graph
+                ck(cudaStreamSynchronize(s), "forward");
+                cudaGraphExecDestroy(h->hg.exec);
+                h->hg = {};
+            }
         }
         }
         ck(cudaStreamSynchronize(s), "forward");
@@ -508,6 +569,7 @@ void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
 struct JVal {
     enum Kind { kNull, kNum, kStr, kObj } kind = kNull;
     double num = 0.0;
+    std::string tok;  // the number's literal (integers are read from it exactly)
     std::string str;
     std::map<std::string, JVal> obj;
 };
@@ -566,17 +628,53 @@ struct JParser {
         while (end < s.size() && std::strchr("+-.0123456789eE", s[end])) ++end;
         if (end == i) bad();
         v.kind = JVal::kNum;
-        v.num = std::stod(s.substr(i, end - i));
+        v.tok = s.substr(i, end - i);
+        v.num = std::stod(v.tok);
         i = end;
         return v;
     }
 };
 
-const JVal& jfield(const JVal& o, const char* k, const std::string& path) {
+// Field access with nlohmann's get<T> semantics (model_io.cpp:146-153, 165-170): a missing key
+// or a value of the wrong JSON kind is a DataError "<path>: <what>: ..."; integers are read
+// exactly from their literal (a fractional literal converts like get<int64_t> on a float).
+const JVal& jfield(const JVal& o, const char* k, const std::string& path, const char* what = "bad header field") {
     auto it = o.obj.find(k);
     if (o.kind != JVal::kObj || it == o.obj.end())
-        fail(CD_ERR_DATA, path + ": bad header field: missing '" + k + "'");
+        fail(CD_ERR_DATA, path + ": " + what + ": key '" + k + "' not found");
     return it->second;
+}
+
+const std::string& jstr(const JVal& o, const char* k, const std::string& path, const char* what = "bad header field") {
+    const JVal& v = jfield(o, k, path, what);
+    if (v.kind != JVal::kStr) fail(CD_ERR_DATA, path + ": " + what + ": '" + k + "' must be a string");
+    return v.str;
+}
+
+double jnum(const JVal& o, const char* k, const std::string& path, const char* what = "bad header field") {
+    const JVal& v = jfield(o, k, path, what);
+    if (v.kind != JVal::kNum) fail(CD_ERR_DATA, path + ": " + what + ": '" + k + "' must be a number");
+    return v.num;
+}
+
+template <typename T>
+T jint(const JVal& o, const char* k, const std::string& path, const char* what = "bad header field") {
+    const JVal& v = jfield(o, k, path, what);
+    if (v.kind != JVal::kNum) fail(CD_ERR_DATA, path + ": " + what + ": '" + k + "' must be a number");
+    if (v.tok.find_first_of(".eE") != std::string::npos) return static_cast<T>(static_cast<long double>(v.num));
+    errno = 0;
+    char* end = nullptr;
+    T out;
+    if (v.tok[0] == '-') {
+        const long long t = std::strtoll(v.tok.c_str(), &end, 10);
+        out = static_cast<T>(t);
+    } else {
+        const unsigned long long t = std::strtoull(v.tok.c_str(), &end, 10);
+        out = static_cast<T>(t);
+    }
+    if (errno == ERANGE || !end || *end != '\0')
+        fail(CD_ERR_DATA, path + ": " + what + ": '" + k + "' is out of range");
+    return out;
 }
 
 void check_finite_blob(const float* p, size_t n, const std::string& path, const char* what) {
@@ -584,22 +682,6 @@ void check_finite_blob(const float* p, size_t n, const std::string& path, const 
         if (!std::isfinite(p[i]))
             fail(CD_ERR_DATA, path + ": " + std::string(what) + " contains a non-finite value at index " +
                                   std::to_string(i));
-}
-
-// One internal stream per device, shared by every handle on it.  The persistent kernels
-// (k_dc_fused, k_mc_fused, k_tc_fused) need all of their CTAs resident at once; two of them
-// running concurrently on different streams could each hold part of the GPU and wait forever
-// for the rest.  Sharing the stream serialises the host-buffer calls of all handles.
-cudaStream_t device_stream(int device) {
-    static std::mutex mu;
-    static std::map<int, cudaStream_t> streams;
-    std::lock_guard<std::mutex> g(mu);
-    auto it = streams.find(device);
-    if (it != streams.end()) return it->second;
-    cudaStream_t s = nullptr;
-    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-    streams.emplace(device, s);
-    return s;
 }
 
 cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_t re, int act,
@@ -625,7 +707,13 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     auto h = std::make_unique<cd_layer>();
     h->device = device;
     h->num_sms = prop.multiProcessorCount;
-    h->stream = device_stream(device);
+    DeviceCtx& ctx = device_ctx(device);
+    std::lock_guard<std::recursive_mutex> dlock(ctx.mu);
+    h->stream = ctx.stream;
+    h->dev_mu = &ctx.mu;
+    for (Grow* g : {&h->tc_ws, &h->blas_ws, &h->g_dx, &h->g_dy, &h->g_dmask_in, &h->g_dmask_out, &h->g_du_in,
+                    &h->g_dind, &h->g_dalive, &h->g_hx, &h->g_hy, &h->g_hmask, &h->g_hind, &h->g_halive})
+        g->gen = &h->gen;
     cdk::LayerDev& L = h->L;
     L.d = d;
     L.F = re - rb;
@@ -644,17 +732,25 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     void* wg = rec + L.ld * esz;
     void* wd = rec + 2 * L.ld * esz;
     float* tmp = nullptr;
-    ck(cudaMalloc(&tmp, sizeof(float) * L.F * d), "cudaMalloc tmp");
+    ck(cudaMalloc(&tmp, sizeof(float) * (L.F * d + 1)), "cudaMalloc tmp");
+    int* nonfinite = reinterpret_cast<int*>(tmp + L.F * d);
+    int bad = 0;
     try {
-        upload_rows(h.get(), w_up, rb, L.F, d, wu, L.ld, L.rs, tmp);
-        upload_rows(h.get(), w_gate, rb, L.F, d, wg, L.ld, L.rs, tmp);
-        upload_rows(h.get(), w_down, rb, L.F, d, wd, L.ld, L.rs, tmp);
+        ck(cudaMemsetAsync(nonfinite, 0, sizeof(int), h->stream), "memset");
+        upload_rows(h.get(), w_up, rb, L.F, d, wu, L.ld, L.rs, tmp, nonfinite);
+        upload_rows(h.get(), w_gate, rb, L.F, d, wg, L.ld, L.rs, tmp, nonfinite);
+        upload_rows(h.get(), w_down, rb, L.F, d, wd, L.ld, L.rs, tmp, nonfinite);
+        ck(cudaMemcpyAsync(&bad, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, h->stream), "upload check");
         ck(cudaStreamSynchronize(h->stream), "upload");
     } catch (...) {
         cudaFree(tmp);
         throw;
     }
     cudaFree(tmp);
+    // The reference accepts non-finite weights (GatedMlpLayer::validate checks shapes only) and
+    // never reads a dead lane's gate / down rows.  The row-union GEMM reads every row, so a
+    // layer holding a non-finite (or bf16-overflowing) weight stays on the CUDA-core kernels.
+    h->weights_finite = bad == 0;
     L.w_up = wu;
     L.w_gate = wg;
     L.w_down = wd;
@@ -673,11 +769,6 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     S.t_count = h->dalloc<unsigned long long>(cdk::kMaxCtas);
     S.t_alive = h->dalloc<unsigned long long>(cdk::kMaxCtas * kMaxBatchFast);
     S.tc_flags = h->dalloc<unsigned>(cdk::kMaxCtas + 64);
-    if (const char* env = std::getenv("CD_DC_CHAIN")) h->use_fused = env[0] != '1';
-    if (const char* env = std::getenv("CD_KEEP0")) h->keep0 = std::atoi(env);
-    if (const char* env = std::getenv("CD_TC")) h->use_tc = env[0] != '0';
-    if (const char* env = std::getenv("CD_HOST_GRAPH")) h->use_host_graph = env[0] != '0';
-    if (const char* env = std::getenv("CD_COPY_KERNEL")) h->mapped_staging = h->mapped_staging && env[0] != '0';
     S.ind = h->dalloc<float>(kMaxBatch * L.F);
     S.ex_s = h->dalloc<float>(kMaxBatch * L.F);
     h->d_x = h->dalloc<float>(kMaxBatch * d);
@@ -754,26 +845,26 @@ int cd_layer_load_cdwn1(int device, const char* path, int dtype, cd_layer** out,
         } catch (const std::exception& e) {
             fail(CD_ERR_DATA, p + ": bad header JSON: " + e.what());
         }
-        const JVal& schema = jfield(h, "schema", p);
-        if (schema.kind != JVal::kStr || schema.str != "v1") fail(CD_ERR_DATA, p + ": unsupported schema");
-        const int64_t d = static_cast<int64_t>(jfield(h, "d_model", p).num);
-        const int64_t F = static_cast<int64_t>(jfield(h, "d_inter", p).num);
-        const std::string act_name = jfield(h, "activation", p).str;
+        if (jstr(h, "schema", p) != "v1") fail(CD_ERR_DATA, p + ": unsupported schema");
+        const int64_t d = jint<int64_t>(h, "d_model", p);
+        const int64_t F = jint<int64_t>(h, "d_inter", p);
+        const std::string act_name = jstr(h, "activation", p);
         int act = -1;
         if (act_name == "silu") act = CD_ACT_SILU;
         else if (act_name == "gelu") act = CD_ACT_GELU_TANH;
         else fail(CD_ERR_DATA, "unknown activation '" + act_name + "' (expected silu|gelu)");
-        const double seed = jfield(h, "seed", p).num;
+        const uint64_t seed = jint<uint64_t>(h, "seed", p);
         if (d <= 0 || F <= 0) fail(CD_ERR_DATA, p + ": non-positive dimensions in header");
         const size_t mat = static_cast<size_t>(d) * static_cast<size_t>(F);
         size_t expected = 3 * mat * 4;
         int64_t r = 0;  // 0: no predictor, -1: ternary (not attached: no B200 path)
         auto pit = h.obj.find("predictor");
         if (pit != h.obj.end() && pit->second.kind == JVal::kObj) {
-            const std::string kind = jfield(pit->second, "kind", p).str;
-            (void)jfield(pit->second, "k", p);
+            const char* pd = "bad predictor descriptor";
+            const std::string kind = jstr(pit->second, "kind", p, pd);
+            (void)jnum(pit->second, "k", p, pd);
             if (kind == "lowrank") {
-                r = static_cast<int64_t>(jfield(pit->second, "d_rank", p).num);
+                r = jint<int64_t>(pit->second, "d_rank", p, pd);
                 if (r <= 0) fail(CD_ERR_DATA, p + ": non-positive predictor rank");
                 expected += (static_cast<size_t>(d) * r + static_cast<size_t>(r) * F) * 4;
             } else if (kind == "ternary") {
@@ -823,7 +914,7 @@ int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, co
         check_layer(h);
         if (d_rank <= 0) fail(CD_ERR_DATA, "make_lowrank_predictor: dims must be positive");
         if (!theta_a || !theta_b) fail(CD_ERR_DATA, "predictor: null theta pointer");
-        std::lock_guard<std::mutex> g(h->mu);
+        CallLock lk(h);
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         cdk::LayerDev& L = h->L;
         const int64_t ldr = round_up(d_rank, cdk::kVecElems);
@@ -851,6 +942,14 @@ int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, co
         if (!h->S.latent) h->S.latent = h->dalloc<float>(kMaxBatch * 2048);
         if (!h->S.ex_lat) h->S.ex_lat = h->dalloc<float>(kMaxBatch * 2048);
         if (!h->S.t_lat) h->S.t_lat = h->dalloc<unsigned long long>(kMaxBatchFast * 2048);
+        // the replaced predictor: its buffers are freed (cudaFree waits for the device) and the
+        // saved host graph, which holds their addresses, is dropped
+        h->dfree(L.theta_a);
+        h->dfree(L.theta_at);
+        h->dfree(L.theta_bt);
+        if (h->hg.exec) cudaGraphExecDestroy(h->hg.exec);
+        h->hg = {};
+        ++h->gen;
         L.r = d_rank;
         L.ldr = ldr;
         L.theta_a = ta;
@@ -860,7 +959,11 @@ int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, co
 }
 
 int cd_layer_destroy(cd_layer* h) {
-    return guarded([&] { delete h; });
+    return guarded([&] {
+        if (!h) return;
+        std::lock_guard<std::recursive_mutex> d(*h->dev_mu);
+        delete h;
+    });
 }
 
 int cd_layer_shape(const cd_layer* h, int64_t* d_model, int64_t* d_inter, int64_t* d_rank, int* dtype,
@@ -1030,7 +1133,7 @@ int cd_predict_logits(cd_layer* h, int64_t batch, const float* x, float* logits)
         check_layer(h);
         if (batch <= 0 || !x || !logits) fail(CD_ERR_DATA, "predict_logits: bad arguments");
         if (!h->L.theta_bt) fail(CD_ERR_DATA, "predict_logits: layer has no low-rank predictor attached");
-        std::lock_guard<std::mutex> g(h->mu);
+        CallLock lk(h);
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         const cdk::LayerDev& L = h->L;
         cdk::LaunchCfg c;
@@ -1062,7 +1165,7 @@ int cd_forward_device(cd_layer* h, int method, int64_t batch, const float* d_x, 
             method != CD_METHOD_CATS)
             fail(CD_ERR_DATA, "unknown method");
         if (d_mask_override && method != CD_METHOD_DC) fail(CD_ERR_DATA, "mask override is DC-only");
-        std::lock_guard<std::mutex> g(h->mu);
+        CallLock lk(h);
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         Req r;
         r.method = method;
@@ -1099,7 +1202,7 @@ int cd_bench_device(cd_layer* h, int method, int64_t batch, const float* x, floa
         if (batch <= 0 || batch > kMaxBatch) fail(CD_ERR_DATA, "bench: batch must be in [1, 32]");
         if (!x || !ns_out || iters <= 0 || warmup < 0) fail(CD_ERR_DATA, "bench: iters must be positive");
         check_reduction(reduction);
-        std::lock_guard<std::mutex> g(h->mu);
+        CallLock lk(h);
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         cudaStream_t s = h->stream;
         ck(cudaMemcpyAsync(h->d_x, x, sizeof(float) * batch * h->L.d, cudaMemcpyHostToDevice, s), "H2D x");
@@ -1151,7 +1254,7 @@ int cd_bench_stages(cd_layer* const* hs, int n_handles, int method, int64_t batc
         cudaError_t err = cudaSuccess;
         for (int64_t it = 0; it < warmup + iters && err == cudaSuccess; ++it) {
             cd_layer* h = hs[it % n_handles];
-            std::lock_guard<std::mutex> g(h->mu);
+            CallLock lk(h);
             Req r;
             r.method = method;
             r.nb = static_cast<int>(batch);
@@ -1191,6 +1294,24 @@ CD_API int cd_debug_timeline(unsigned long long* out, int64_t n) {
     });
 }
 #endif
+
+int cd_layer_set_engines(cd_layer* h, int engines) {
+    return guarded([&] {
+        check_layer(h);
+        if (engines & ~(CD_ENGINE_FUSED | CD_ENGINE_TENSOR | CD_ENGINE_HOST_GRAPH))
+            fail(CD_ERR_DATA, "set_engines: unknown engine flag");
+        CallLock lk(h);
+        h->use_fused = (engines & CD_ENGINE_FUSED) != 0;
+        h->use_tc = (engines & CD_ENGINE_TENSOR) != 0;
+        h->use_host_graph = (engines & CD_ENGINE_HOST_GRAPH) != 0;
+        if (h->hg.exec) {
+            ck(cudaStreamSynchronize(h->stream), "sync");
+            cudaGraphExecDestroy(h->hg.exec);
+        }
+        h->hg = {};
+        ++h->gen;
+    });
+}
 
 int cd_layer_sync(cd_layer* h) {
     return guarded([&] {

@@ -93,13 +93,12 @@ cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, 
                                const float* x, int nb, float* y, int* alive_out,
                                const LaunchCfg& c);
 // D-CountDown step as one persistent kernel (kernels_fused.cu): latent, predictor, threshold,
-// compaction and the sparse FFN with grid barriers; zeroes and accumulates y, writes
-// alive_out.  keep0: active neurons of its own chunk each CTA streams before the global
-// rebalancing.  Returns cudaErrorInvalidValue for shapes it does not cover (the caller then
+// compaction and the sparse FFN (work-stealing schedule); zeroes and accumulates y, writes
+// alive_out.  Returns cudaErrorInvalidValue for shapes it does not cover (the caller then
 // uses the three-kernel chain).
 cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
                             const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
-                            int* alive_out, const LaunchCfg& c, int keep0 = 3);
+                            int* alive_out, const LaunchCfg& c);
 // M-CountDown step (batch 1) as one persistent kernel (kernels_fused_mc.cu): dense u = W_up x
 // over each CTA's neuron chunk, |u| > tau, compaction, and the sparse gate / down stage with
 // the work-stealing schedule.  Zeroes and accumulates y; optional mask / u / alive outputs.
@@ -136,6 +135,9 @@ cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float
 
 // dst[0, bytes) = src[0, bytes) by a kernel (either side may be mapped pinned host memory).
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
+// *out += number of values of v[0, n) that are non-finite or overflow bf16 (upload check).
+cudaError_t launch_count_nonfinite(const float* v, int64_t n, int* out, cudaStream_t s);
 
 // One-thread kernel that occupies the stream for `ns` nanoseconds (timing helper).
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t s);

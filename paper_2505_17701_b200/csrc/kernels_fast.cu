@@ -759,7 +759,24 @@ __global__ void k_copy_bytes(uint8_t* __restrict__ dst, const uint8_t* __restric
     }
 }
 
+// Upload check: counts f32 values that are not finite or overflow bf16 (|v| rounds to inf).
+__global__ void k_count_nonfinite(const float* __restrict__ v, int64_t n, int* __restrict__ out) {
+    int bad = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        bad += !(fabsf(v[i]) < 3.3961e38f);  // NaN compares false
+    bad = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(bad));
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(out, bad);
+}
+
 // ---------------------------------------------------------------- public launchers
+cudaError_t launch_count_nonfinite(const float* v, int64_t n, int* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = (n + 255) / 256;
+    k_count_nonfinite<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(v, n, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     if (bytes == 0) return cudaSuccess;
     const size_t blocks = (bytes + 256 * 16 - 1) / (256 * 16);

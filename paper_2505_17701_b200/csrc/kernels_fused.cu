@@ -65,7 +65,7 @@ struct FusedParams {
     float* logits_out;
     int* alive_out;
     float tau;
-    int nb, nstages, rows_per_cta, keep0, qrows;
+    int nb, nstages, rows_per_cta, qrows;
     int b_smem;  // bf16: predictor rows staged by TMA in the ring, moved to registers after stage 1
 };
 
@@ -121,8 +121,6 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
     const int q0 = blockIdx.x * qrows;                      // this CTA's latent columns [q0, q1)
     const int q1 = min(static_cast<int>(L.r), q0 + qrows);
     const int nq = q1 > q0 ? q1 - q0 : 0;
-    // the kept records are issued into a fresh ring: never more than it holds
-    // (P.keep0 is unused: the own-work cap comes from the previous launch)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < nstages; ++s) {
@@ -588,7 +586,7 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
 #pragma unroll
                     for (int j = 0; j < VPT; ++j) {
                         const int vec = ct + j * nc;
-                        if (vec < nvec && P.keep0 != -1) {
+                        if (vec < nvec) {
                             float wg[8], wu[8];
                             Vec8<W>::load(rgate + vec * kVec, wg);
                             Vec8<W>::load(rup + vec * kVec, wu);
@@ -639,7 +637,7 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
 #pragma unroll
                     for (int j = 0; j < VPT; ++j) {
                         const int vec = ct + j * nc;
-                        if (vec < nvec && P.keep0 != -1) {
+                        if (vec < nvec) {
                             float wd[8];
                             Vec8<W>::load(rdown + vec * kVec, wd);
 #pragma unroll
@@ -717,7 +715,7 @@ cudaError_t read_timeline_fused(unsigned long long*, int64_t) { return cudaError
 
 cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
                             const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
-                            int* alive_out, const LaunchCfg& c, int keep0) {
+                            int* alive_out, const LaunchCfg& c) {
     if (!L.theta_at || !S.t_lat || !S.t_list || !S.t_count || !S.t_alive || !S.ctl) return cudaErrorInvalidValue;
     if (c.num_sms >= kYZeroWord || L.F >= (1 << 27)) return cudaErrorInvalidValue;
     // x rows are staged by the TMA engine: 16-byte aligned rows of a multiple of 16 bytes
@@ -750,10 +748,7 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
     const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
     if (nstages < 2) return cudaErrorInvalidValue;
-    static const bool bsmem_env = [] {
-        const char* e = std::getenv("CD_DC_BSMEM");
-        return !(e && e[0] == '0');
-    }();
+    static const bool bsmem_env = dev_knob("CD_DC_BSMEM", 1) != 0;
     const int b_smem = regb && bsmem_env && (int64_t)rpc * brow_bytes + aux_bytes <= stage_bytes * nstages ? 1 : 0;
     if (regb ? rpc > nwc * 8 : (int64_t)rpc * brow_bytes + aux_bytes > stage_bytes * nstages)
         return cudaErrorInvalidValue;  // register path: <= 8 predictor rows per consumer warp
@@ -775,7 +770,6 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
         p.nb = nb;
         p.nstages = nstages;
         p.rows_per_cta = rpc;
-        p.keep0 = keep0;
         p.qrows = qrows;
         p.b_smem = b_smem;
         return launch_ex(kern, dim3(G), dim3(threads), smem, c, true, p);

@@ -476,10 +476,7 @@ cudaError_t launch_mc_fused(const LayerDev& L, const Scratch& S, const float* x,
         // W_up stage loads as one 3-D tensor copy: [rows][ld / inner][inner], no swizzle (the smem
         // image is the plain row-major 3 x ld block the consumers read)
         p.use_map = 0;
-        static const bool map_env = [] {
-            const char* e = std::getenv("CD_MC_TMAP");
-            return !(e && e[0] == '0');
-        }();
+        static const bool map_env = dev_knob("CD_MC_TMAP", 1) != 0;
         int inner = 0;
         for (int cand : {256, 128, 64, 32, 16, 8})
             if (L.ld % cand == 0 && L.ld / cand <= 256) { inner = cand; break; }

@@ -619,10 +619,7 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
                            float* ind_out, int* alive_out, const LaunchCfg& c) {
     if (L.dtype != 1 /* bf16 */ || !L.w_up) return cudaErrorInvalidValue;
     if (method == kDC && !ovr && !L.theta_bt) return cudaErrorInvalidValue;
-    static const bool fused_env = [] {
-        const char* e = std::getenv("CD_TC_FUSED");
-        return !(e && e[0] == '0');
-    }();
+    static const bool fused_env = dev_knob("CD_TC_FUSED", 1) != 0;
     if (p.split && fused_env)
         return launch_batched_fused(L, p, ws, workspace_bytes(L, p, c.num_sms), flags, method, nb, x, tau, ovr, y,
                                     mask_out, ind_out, alive_out, c);
@@ -675,10 +672,7 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     a.kb_x = static_cast<int>((L.d + kBK - 1) / kBK);
     a.kb_z = dc_pred ? static_cast<int>((L.r + kBK - 1) / kBK) : 0;
     a.tau = tau;
-    static const int st_env = [] {
-        const char* e = std::getenv("CD_TC_STAGES");
-        return e ? std::atoi(e) : 0;
-    }();
+    static const int st_env = dev_knob("CD_TC_STAGES", 0);
     a.ovr = ovr;
     a.s_out = sb;
     a.ld_s = ld_s;
@@ -691,10 +685,7 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     a.n_tiles = p.n_tiles;
     a.tiles = static_cast<int>((L.F + kBM - 1) / kBM) * p.n_tiles;
     const int64_t units = static_cast<int64_t>(a.tiles) * (a.kb_x + a.kb_z);
-    static const int grid_env = [] {
-        const char* e = std::getenv("CD_TC_GRID");
-        return e ? std::atoi(e) : 0;
-    }();
+    static const int grid_env = dev_knob("CD_TC_GRID", 0);
     static unsigned long long* tl_env = []() -> unsigned long long* {
 #ifdef CD_TIMELINE  // development builds only: a device address taken from the environment
         const char* e = std::getenv("CD_TC_TL");

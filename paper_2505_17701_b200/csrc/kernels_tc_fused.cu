@@ -675,10 +675,7 @@ cudaError_t launch_batched_fused(const LayerDev& L, const Plan& p, void* ws_base
 #endif
     }();
     a.tl = tl_env;
-    static const int pf_env = [] {
-        const char* e = std::getenv("CD_TC_PB_PF");
-        return e ? std::atoi(e) : 0;
-    }();
+    static const int pf_env = dev_knob("CD_TC_PB_PF", 0);
     a.pb_pf = pf_env;
     const int cols_used = dc_pred ? 3 * p.N : 2 * p.N;
     a.tmem_cols = cols_used <= 64 ? 64 : cols_used <= 128 ? 128 : cols_used <= 256 ? 256 : 512;

@@ -2,6 +2,8 @@
 // dependent launch, dynamic shared-memory opt-in).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <mutex>
@@ -10,6 +12,18 @@
 #include "kernels.h"
 
 namespace cdk {
+
+// Development knobs: read from the environment only in the -DCD_TIMELINE development build
+// (make TIMELINE=1); release builds always take the default.
+inline int dev_knob(const char* name, int dflt) {
+#ifdef CD_TIMELINE
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
+}
 
 constexpr size_t kMaxDynSmem = 227 * 1024;
 

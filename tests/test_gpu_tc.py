@@ -151,16 +151,16 @@ def test_tc_dense_and_prefill(oracle, B):
         assert rel_l2(y[b], oracle.forward_dense(g, X[b])["y"]) <= tol
 
 
-def test_tc_matches_cuda_core_path(oracle, monkeypatch):
-    """Same batch through the tensor cores and (CD_TC=0) the CUDA-core fused chain."""
+def test_tc_matches_cuda_core_path(oracle):
+    """Same batch through the tensor cores and (tensor engine off) the CUDA-core fused chain."""
     seed, d, F, r = 202, 200, 300, 40
     g, _, _ = make(oracle, seed, d, F, r)
     X = batch(oracle, 3, 16, d)
     outs = {}
     for tc in ("1", "0"):
-        monkeypatch.setenv("CD_TC", tc)
         layer = cd.GatedMlpLayer(d, F, 0, g["w_up"], g["w_gate"], g["w_down"], device_dtype="bf16")
         pred = cd.Predictor(cd.LowRankPredictor(d, r, F, g["theta_a"], g["theta_b"]), "bf16")
+        layer.device_layer(pred).set_engines(tensor=(tc == "1"))
         outs[tc] = cd.pipeline_dc(layer, X, pred, FAST, tau_d=0.05, want_logits=True)
         assert layer.device_layer(pred).last_path() == ("tensor" if tc == "1" else "fast")
     for b in range(16):

@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--no-sweep", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-batched", action="store_true", help="skip BASELINE configs[4] (batch-64 + prefill)")
+    p.add_argument("--no-configs", action="store_true", help="skip configs[2] (Gemma) and the f32 line")
     return p.parse_args()
 
 
@@ -155,7 +156,7 @@ def tensor_peak():
     return 1376.5, "fallback"
 
 
-def batched_section(torch, cd, stream, steps, peak_gbs):
+def batched_section(torch, cd, timer, steps, peak_gbs):
     """BASELINE.json configs[4]: Qwen2.5-14B FFN shape (d=5120, d_ff=13824, SiLU), batch-64 decode at
     ~80% sparsity (per-sample masks, D- and M-CountDown) and a dense prefill of 2048 tokens, on the
     tcgen05 tensor-core path (kernels_tc.cu).  Weights 3 x 13824 x 5120 bf16 = 425 MB > L2, so every
@@ -189,17 +190,16 @@ def batched_section(torch, cd, stream, steps, peak_gbs):
         def fwd(i, cs, method=method, nb=nb, x=x, y=y, alive=alive, tau=tau):
             dev.forward_device(method, x, y, tau=tau, batch=nb, alive_out=alive, stream=cs)
 
-        with torch.cuda.stream(stream):
+        with torch.cuda.stream(timer.stream):
             for i in range(3):
-                fwd(i, stream.cuda_stream)
+                fwd(i, timer.stream.cuda_stream)
         torch.cuda.synchronize()
         path = dev.last_path()
         n = steps if nb <= 64 else max(3, steps // 8)
-        ms, g = graph_rate(torch, fwd, n, stream)
-        del g
-        us = 1e3 * ms / n
+        ms, n_timed, _ = timer.run(fwd, n)
+        us = 1e3 * ms
         sp = 1.0 - alive.float().mean().item() / Fq
-        case = {"case": name, "batch": nb, "path": path, "us_per_step": round(us, 2),
+        case = {"case": name, "batch": nb, "path": path, "us_per_step": round(us, 2), "timed_steps": n_timed,
                 "tokens_per_s": round(nb / us * 1e6, 1), "realized_sparsity": round(sp, 4)}
         if nb <= 64:
             pbytes = (Dq * Rq + Fq * Rq) * 2 if method == _capi.METHOD_DC else 0
@@ -237,6 +237,10 @@ def cpu_baseline_sample():
 
 
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref, the unmodified library) on the same
+    layer, inputs and alive sets.  Only oracle/ is loaded here (the reference arm must not load
+    the product library): inputs come from the reference's own Rng (normal_f == float(normal()),
+    numerics.hpp:50-52), thresholds from its predict_logits and alive_count_for."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -245,11 +249,10 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcountdown_ref.so not built"}))
         return
     ref = O.Reference()
-    import paper_2505_17701_b200 as cd  # host-only helpers (synthetic normals), no device use
     g = ref.generate(SEED, D, F, R)
-    xcal = np.stack([cd.synth_normals(10_000 + i, D) for i in range(N_CAL)])
-    xs = np.stack([cd.synth_normals(1_000 + i, D) for i in range(N_X)])
-    m = cd.alive_count_for(args.k, F)
+    xcal = np.stack([ref.rng_normals(10_000 + i, D).astype(np.float32) for i in range(N_CAL)])
+    xs = np.stack([ref.rng_normals(1_000 + i, D).astype(np.float32) for i in range(N_X)])
+    m = ref.alive_count_for(args.k, F)
     taus = []
     for x in xcal:
         z = ref.predict_logits(g["theta_a"], g["theta_b"], x)
@@ -285,26 +288,232 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- ours
-def graph_rate(torch, fwd, steps, stream, reps_soak=0):
-    """Capture `steps` decode steps in one CUDA graph; return (ms for one replay, graph)."""
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(stream):
-        with torch.cuda.graph(g, stream=stream):
-            cs = torch.cuda.current_stream().cuda_stream
-            for i in range(steps):
-                fwd(i, cs)
-    g.replay()
+class Timer:
+    """Steady-state device timing of a captured step sequence: a graph of `steps` steps is
+    replayed back to back until the timed region lasts >= min_ms (so the rate does not depend
+    on --steps: graph launch and the first step's unoverlapped prologue are amortised), CUDA
+    events on the launching stream, barrier + synchronize on both sides, max over ranks."""
+
+    def __init__(self, torch, stream, dist=None, min_ms=60.0):
+        self.torch, self.stream, self.dist, self.min_ms = torch, stream, dist, min_ms
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, v):
+        if self.dist is None:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def capture(self, fwd, steps):
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(self.stream):
+            with torch.cuda.graph(g, stream=self.stream):
+                cs = torch.cuda.current_stream().cuda_stream
+                for i in range(steps):
+                    fwd(i, cs)
+        return g
+
+    def replay_ms(self, g, reps):
+        torch = self.torch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.barrier()
+        e0.record(self.stream)
+        with torch.cuda.stream(self.stream):
+            for _ in range(reps):
+                g.replay()
+        e1.record(self.stream)
+        self.barrier()
+        return self.max_over_ranks(e0.elapsed_time(e1))
+
+    def run(self, fwd, steps, soak_s=0.0):
+        """-> (ms per step, timed steps, replays).  Same replay count on every rank."""
+        g = self.capture(fwd, steps)
+        one = self.replay_ms(g, 1)
+        reps = max(2, int(np.ceil(self.min_ms / max(one, 1e-3))))
+        if soak_s > 0:
+            self.replay_ms(g, max(1, int(soak_s * 1e3 / max(one, 1e-3))))
+        ms = self.replay_ms(g, reps)
+        del g
+        return ms / (reps * steps), reps * steps, reps
+
+
+def exact_logits(cd, pred, xs):
+    """Predictor logits from the exact kernels (DeterministicOrdered: bitwise the reference's
+    predict_logits, pinned by tests/test_gpu_parity.py)."""
+    return np.atleast_2d(cd.predict_logits(pred, xs))
+
+
+def top_m_tau(rows, m):
+    """Mean over samples of each sample's exact top-m threshold (calibration.cpp:11-37:
+    the (m+1)-th largest value, ties to the lower index, numerics.cpp:105-142)."""
+    n = rows.shape[1]
+    return float(np.mean([row[np.lexsort((np.arange(n), -row))[m]] if m < n else -np.inf for row in rows]))
+
+
+def flip_report(torch, cd, dev, method, xs, tau, z_exact, band=1e-6):
+    """Near-threshold flips of the fast path's index sets against the exact indicator
+    (north_star: index sets equal except lanes whose coefficient lies within 1e-6 relative of
+    the threshold -- counted and reported).  The fast path's own indicator (logits / u) is
+    returned by the same kernel and compared too."""
+    B, Fx = z_exact.shape
+    mask = torch.zeros((B, Fx), dtype=torch.uint8, device="cuda")
+    ind = torch.zeros((B, Fx), dtype=torch.float32, device="cuda")
+    y = torch.zeros((B, xs.shape[1]), device="cuda")
+    xd = torch.from_numpy(np.ascontiguousarray(xs)).cuda()
+    for b in range(B):
+        dev.forward_device(method, xd[b], y[b], tau=tau, batch=1, mask_out=mask[b], indicator_out=ind[b])
     torch.cuda.synchronize()
-    for _ in range(reps_soak):
-        g.replay()
+    got = mask.cpu().numpy().astype(bool)
+    zf = ind.cpu().numpy()
+    ref = np.abs(z_exact) if method == cd._capi.METHOD_MC else z_exact
+    want = ref > np.float32(tau)
+    flips = got != want
+    dist = np.abs(ref[flips].astype(np.float64) - tau) / max(abs(tau), 1e-30)
+    return {"inputs": int(B), "lanes": int(B * Fx), "flips": int(flips.sum()),
+            "flips_outside_1e-6": int((dist > band).sum()),
+            "max_rel_dist_of_flip": float(dist.max()) if dist.size else 0.0,
+            "indicator_max_abs_err_rel_tau": float(np.max(np.abs(
+                (np.abs(zf) if method == cd._capi.METHOD_MC else zf) - ref)) / max(abs(tau), 1e-30)),
+            "note": "fast-path mask vs exact-kernel indicator > tau (exact == reference bitwise)"}
+
+
+def gemma_section(torch, cd, timer, steps, peak_gbs):
+    """BASELINE.json configs[2]: Gemma-2-9B FFN (d=3584, d_ff=14336, GeLU-tanh), r=512, bf16
+    weights, batch 1 / 4 / 16 decode, M- and D-CountDown at 90% (per-sample masks; the bytes of
+    a batched step are the UNION of the samples' active rows).  4 layer replicas rotate per
+    step so the touched rows exceed L2."""
+    from paper_2505_17701_b200 import costmodel as cm
+    Dg, Fg, Rg, NL = 3584, 14336, 512, 4
+    layers = []
+    for i in range(NL):
+        layer, _, pred = cd.synth_workload(SEED + 100 + i, Dg, Fg, Rg, activation=cd.Activation.GeluTanh,
+                                           device_dtype="bf16")
+        layers.append((layer, pred, layer.device_layer(pred)))
+    layer0, pred0, _ = layers[0]
+    xcal = np.stack([cd.synth_normals(50_000 + i, Dg) for i in range(16)])
+    xs = np.stack([cd.synth_normals(60_000 + i, Dg) for i in range(16)])
+    m = cd.alive_count_for(0.9, Fg)
+    z_cal = exact_logits(cd, pred0, xcal)
+    z_x = exact_logits(cd, pred0, xs)
+    tau_dc = top_m_tau(z_cal, m)
+    u_cal = np.abs(cd.pipeline_mc(layer0, xcal, float("inf"), cd.BlockConfig(
+        reduction=cd.Reduction.DeterministicOrdered), want_u=True).u)
+    u_x = np.abs(cd.pipeline_mc(layer0, xs, float("inf"), cd.BlockConfig(
+        reduction=cd.Reduction.DeterministicOrdered), want_u=True).u)
+    tau_mc = top_m_tau(u_cal, m)
+    xd = torch.from_numpy(xs).cuda()
+    out = {"workload": "BASELINE configs[2]: gemma-2-9b FFN d=3584 d_ff=14336 GeLU-tanh r=512, bf16 weights, "
+                       "k=0.9 (tau calibrated on 16 inputs), per-sample masks, 4 layer replicas rotated",
+           "cases": []}
+    for method, name, tau, ind in ((cd._capi.METHOD_DC, "dc", tau_dc, z_x), (cd._capi.METHOD_MC, "mc", tau_mc, u_x)):
+        for B in (1, 4, 16):
+            y = torch.zeros((NL, B, Dg), device="cuda")
+            nx = 16 // B
+
+            def fwd(i, cs, method=method, B=B, y=y, tau=tau, nx=nx):
+                li, xi = i % NL, (i // NL) % nx
+                layers[li][2].forward_device(method, xd[xi * B:(xi + 1) * B], y[li], tau=tau, batch=B, stream=cs)
+
+            with torch.cuda.stream(timer.stream):
+                for i in range(2 * NL):
+                    fwd(i, timer.stream.cuda_stream)
+            torch.cuda.synchronize()
+            path = layers[0][2].last_path()
+            ms, n_timed, _ = timer.run(fwd, max(steps, 2 * NL))
+            us = 1e3 * ms
+            alive = ind > np.float32(tau)
+            unions = [int(np.any(alive[j * B:(j + 1) * B], axis=0).sum()) for j in range(nx)]
+            per = [int(a) for a in alive.sum(axis=1)]
+            s_u = float(np.mean(unions))
+            bytes_ = cm.device_bytes(name, Dg, Fg, Rg if name == "dc" else 0, int(round(s_u)), 2)["total_bytes"]
+            bytes_ += (B - 1) * 8 * Dg  # the other samples' x / y
+            out["cases"].append({
+                "method": name, "batch": B, "path": path, "us_per_step": round(us, 3),
+                "tokens_per_s": round(B / us * 1e6, 1), "realized_sparsity": round(1 - float(np.mean(per)) / Fg, 4),
+                "union_rows": round(s_u, 1), "timed_steps": n_timed,
+                "roofline": {"bound": "hbm", "alg_bytes": bytes_, "achieved": round(bytes_ / us / 1e3, 1),
+                             "peak": peak_gbs, "unit": "GB/s", "frac": round(bytes_ / us / 1e3 / peak_gbs, 4)}})
+    dense_y = torch.zeros((NL, Dg), device="cuda")
+
+    def fwd_dense(i, cs):
+        layers[i % NL][2].forward_device(cd._capi.METHOD_DENSE, xd[i % 16], dense_y[i % NL], batch=1, stream=cs)
+
+    ms, n_timed, _ = timer.run(fwd_dense, max(steps, 2 * NL))
+    bytes_ = 3 * Fg * Dg * 2 + 8 * Dg
+    out["cases"].append({"method": "dense", "batch": 1, "us_per_step": round(1e3 * ms, 3),
+                         "tokens_per_s": round(1e6 / (1e3 * ms), 1), "timed_steps": n_timed,
+                         "roofline": {"bound": "hbm", "alg_bytes": bytes_, "achieved": round(bytes_ / (1e3 * ms) / 1e3, 1),
+                                      "peak": peak_gbs, "unit": "GB/s",
+                                      "frac": round(bytes_ / (1e3 * ms) / 1e3 / peak_gbs, 4)}})
+    del layers
+    return out
+
+
+def f32_section(torch, cd, timer, steps, peak_gbs, k):
+    """The headline workload at the reference's own precision (f32 weights, f32 arithmetic,
+    numerics.cpp:77-87): same layer, inputs and tau_D as the headline, so the CPU arm compares
+    like for like.  Device rate (2 replicas rotated: 2 x 112 MB touched > L2) and e2e through
+    cd_pipeline_dc with host buffers; flips of the fast path's index sets vs the exact kernels
+    (the "fp32 oracle mode", bitwise the reference)."""
+    from paper_2505_17701_b200 import costmodel as cm
+    from paper_2505_17701_b200._capi import lib, ptr, check
+    NL = 2
+    layer, _, pred = cd.synth_workload(SEED, D, F, R, device_dtype="f32")
+    devs = [layer.device_layer(pred)]
+    for _ in range(NL - 1):
+        d2 = cd.DeviceLayer.create(layer.w_up, layer.w_gate, layer.w_down, 0, "f32")
+        d2.set_predictor(pred.lowrank())
+        devs.append(d2)
+    xcal = np.stack([cd.synth_normals(10_000 + i, D) for i in range(N_CAL)])
+    xs = np.stack([cd.synth_normals(1_000 + i, D) for i in range(N_X)])
+    z_cal = exact_logits(cd, pred, xcal)
+    z_x = exact_logits(cd, pred, xs)
+    tau = top_m_tau(z_cal, cd.alive_count_for(k, F))
+    xd = torch.from_numpy(xs).cuda()
+    y = torch.zeros((NL, D), device="cuda")
+
+    def fwd(i, cs):
+        devs[i % NL].forward_device(cd._capi.METHOD_DC, xd[i % N_X], y[i % NL], tau=tau, batch=1, stream=cs)
+
+    with torch.cuda.stream(timer.stream):
+        for i in range(2 * NL):
+            fwd(i, timer.stream.cuda_stream)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    with torch.cuda.stream(stream):
-        g.replay()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1), g
+    launches = devs[0].last_launches()
+    ms, n_timed, _ = timer.run(fwd, max(steps, 2 * NL))
+    alive = (z_x > np.float32(tau)).sum(axis=1)
+    bytes_ = float(np.mean([cm.device_bytes("dc", D, F, R, int(a), 4)["total_bytes"] for a in alive]))
+    # e2e: the reference-facing call with host buffers
+    L = lib()
+    yh = np.empty(D, np.float32)
+    ah = np.empty(1, np.int64)
+    xs_c = [np.ascontiguousarray(x) for x in xs]
+    for i in range(3 * NL):
+        check(L.cd_pipeline_dc(devs[i % NL].raw, 1, ptr(xs_c[i % N_X]), tau, None, 1, ptr(yh), None, ptr(ah), None))
+    n = max(steps, 64)
+    t0 = time.perf_counter()
+    for i in range(n):
+        check(L.cd_pipeline_dc(devs[i % NL].raw, 1, ptr(xs_c[i % N_X]), tau, None, 1, ptr(yh), None, ptr(ah), None))
+    dt = time.perf_counter() - t0
+    flips = flip_report(torch, cd, devs[0], cd._capi.METHOD_DC, xs, tau, z_x)
+    out = {"workload": f"headline config at f32 (the reference's precision): llama3.1-8b FFN, D-CountDown r={R} "
+                       f"k={k}, batch 1, f32 weights / arithmetic, same inputs and tau_D",
+           "value": round(1e3 / ms, 1), "unit": "tokens/s", "us_per_step": round(1e3 * ms, 3), "timed_steps": n_timed,
+           "kernels_per_step": launches, "realized_sparsity": round(1 - float(alive.mean()) / F, 4),
+           "roofline": {"bound": "hbm", "alg_bytes": bytes_, "achieved": round(bytes_ / ms / 1e6, 1), "peak": peak_gbs,
+                        "unit": "GB/s", "frac": round(bytes_ / ms / 1e6 / peak_gbs, 4)},
+           "e2e": {"value": round(n / dt, 1), "unit": "tokens/s", "calls": n, "h2d_bytes_per_step": 4 * D,
+                   "d2h_bytes_per_step": 4 * D + 4, "api": "cd_pipeline_dc (host buffers), wall clock"},
+           "flips": flips}
+    del devs
+    layer.invalidate()
+    return out
 
 
 def run_ours(args):
@@ -322,24 +531,22 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, peak_kind = peaks()
+    stream = torch.cuda.Stream()
+    timer = Timer(torch, stream, dist)
 
     layer, pred, xcal, xs = workload()
-    # thresholds: tau_D per k (calibrated with the exact kernels on the full layer's logits)
     m_of = lambda k: cd.alive_count_for(k, F)
-    z_cal = np.atleast_2d(cd.predict_logits(pred, xcal))
-    z_x = np.atleast_2d(cd.predict_logits(pred, xs))
+    z_cal = exact_logits(cd, pred, xcal)
+    z_x = exact_logits(cd, pred, xs)
 
     def tau_dc(k):
-        m = m_of(k)
-        return float(np.mean([row[np.lexsort((np.arange(F), -row))[m]] for row in z_cal]))
+        return top_m_tau(z_cal, m_of(k))
 
     NL = args.layers
     tps = [TPLayer(layer, pred, world, rank, device=local, device_dtype="bf16") for _ in range(NL)]
     devs = [t.dev for t in tps]
     x_dev = torch.from_numpy(xs).cuda()
     y_dev = torch.zeros((NL, N_X, D), device="cuda")
-    alive_dev = torch.zeros((NL * N_X,), dtype=torch.int32, device="cuda")
-    stream = torch.cuda.Stream()
 
     def step_fn(method, tau, comm=True):
         def f(i, cs):
@@ -349,23 +556,8 @@ def run_ours(args):
                 allreduce_sum_(y_dev[li, xi])
         return f
 
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def max_over_ranks(v):
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     rb, re_ = tps[0].rows
     Fl = re_ - rb
-
-    def alive_of(tau):
-        return (z_x[:, rb:re_] > np.float32(tau)).sum(axis=1)  # this rank's alive rows per input
 
     def chain_bytes(method, alive_local):
         return cm.device_bytes(method, D, Fl, R if method == "dc" else 0, int(alive_local), 2)["total_bytes"]
@@ -374,115 +566,103 @@ def run_ours(args):
     tau = tau_dc(args.k)
     fwd = step_fn(cd._capi.METHOD_DC, tau)
     with torch.cuda.stream(stream):
-        for i in range(args.warmup):
+        for i in range(max(args.warmup, 2 * NL)):
             fwd(i, stream.cuda_stream)
     torch.cuda.synchronize()
     vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
     clk = ClockSampler(int(vis[local]) if len(vis) > local and vis[local].strip().isdigit() else local)
     with clk:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            with torch.cuda.graph(g, stream=stream):
-                cs = torch.cuda.current_stream().cuda_stream
-                for i in range(args.steps):
-                    fwd(i, cs)
-        for _ in range(max(3, int(0.6e3 / max(1e-3, 0.012 * args.steps)))):  # ~0.6 s soak
-            g.replay()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        with torch.cuda.stream(stream):
-            g.replay()
-        e1.record(stream)
-        barrier()
-        ms = max_over_ranks(e0.elapsed_time(e1))
+        ms_step, n_timed, reps = timer.run(fwd, args.steps, soak_s=0.6)
     launches_per_step = devs[0].last_launches()
-    value = args.steps / (ms / 1e3)
-    alive_x = alive_of(tau)
+    value = 1e3 / ms_step
+    alive_x = (z_x[:, rb:re_] > np.float32(tau)).sum(axis=1)
     alive_full = (z_x > np.float32(tau)).sum(axis=1)
     realized = 1.0 - float(alive_full.mean()) / F
     bytes_step = float(np.mean([chain_bytes("dc", a) for a in alive_x]))
-    del g
 
-    # ---- dominant kernel roofline: per-stage device times (PDL off, events between kernels)
+    # ---- dominant kernel: one launch per step (the fused persistent kernel), so its average
+    # launch duration over the timed region is the region time / timed launches; the isolated
+    # launch (PDL off, events around it, prologue not overlapped) is kept for reference
     st_iters = 64
     stage_ns = cd.DeviceLayer.bench_stages(devs, cd._capi.METHOD_DC, x_dev[0], tau, 8, st_iters)
     a0 = int(alive_x[0])
     if len(stage_ns) == 1:
-        # the fused persistent kernel: the whole step's algorithmic bytes (theta_a, theta_b,
-        # three rows per alive neuron, x in, y out)
         stage_bytes = [chain_bytes("dc", a0)]
         names = ["k_dc_fused"]
     else:
-        stage_bytes = [D * R * 2 + 4 * D + 4 * R,          # latent: theta_a + x + latent
-                       Fl * R * 2 + 4 * R + 4 * D,          # indicator: theta_bt + latent (+ y zeroing)
-                       3 * a0 * D * 2 + 4 * D * 2 + 8 * a0]  # sparse: 3 rows per alive neuron + x, y, list
+        stage_bytes = [D * R * 2 + 4 * D + 4 * R, Fl * R * 2 + 4 * R + 4 * D, 3 * a0 * D * 2 + 4 * D * 2 + 8 * a0]
         names = ["k_latent_fast", "k_indicator_dc", "k_sparse<DC>"]
     dom = int(np.argmax(stage_ns))
-    stages = [{"kernel": n, "us": ns / 1e3, "alg_bytes": b, "gbs": b / ns}
+    stages = [{"kernel": n, "us_isolated": ns / 1e3, "alg_bytes": b, "gbs": b / ns}
               for n, ns, b in zip(names, stage_ns, stage_bytes)]
     if len(stage_ns) == 1 and world == 1:
-        # one launch per step: the kernel's average launch duration over the timed region is the
-        # region time / steps (CUDA events around the graph, same stream); the isolated launch
-        # (PDL off, cold prologue) is kept in `stages` for reference
-        launch_ns = 1e6 * ms / args.steps
-        roof_how = f"CUDA events over the timed region: {args.steps} launches of {names[0]}, 1 per step"
-        stages[0]["note"] = "isolated launch (PDL off, events around it, prologue not overlapped)"
+        launch_ns = 1e6 * ms_step
+        alg = bytes_step
+        roof_how = (f"CUDA events over the timed region: {n_timed} launches of {names[0]} ({reps} replays of a "
+                    f"{args.steps}-step graph), 1 per step; alg bytes = mean over the {N_X} inputs' realized "
+                    f"active counts")
     else:
         launch_ns = stage_ns[dom]
+        alg = stage_bytes[dom]
         roof_how = "per-kernel CUDA events (bench_stages: PDL off, an event after every launch)"
-    achieved = stage_bytes[dom] / launch_ns  # bytes/ns == GB/s
+    achieved = alg / launch_ns  # bytes/ns == GB/s
+    flips = flip_report(torch, cd, devs[0], cd._capi.METHOD_DC, xs, tau, z_x) if world == 1 else None
 
-    # ---- e2e through the C-ABI with host buffers (rank 0's view; TP adds the all-reduce)
+    # ---- e2e through the C-ABI with host buffers (rank 0's view)
     e2e = None
     if world == 1:
-        import ctypes as C
         from paper_2505_17701_b200._capi import lib, ptr, check
         L = lib()
         yh = np.empty(D, np.float32)
         ah = np.empty(1, np.int64)
         xs_c = [np.ascontiguousarray(x) for x in xs]
-        for i in range(args.warmup):
-            check(L.cd_pipeline_dc(devs[i % NL].raw, 1, ptr(xs_c[i % N_X]), tau, None, 1, ptr(yh), None, ptr(ah), None))
+
+        def call(i):
+            check(L.cd_pipeline_dc(devs[i % NL].raw, 1, ptr(xs_c[i % N_X]), tau, None, 1, ptr(yh), None, ptr(ah),
+                                   None))
+
+        # every rotated handle captures its host graph on its 2nd identical call: warm them all
+        for i in range(max(args.warmup, 3 * NL)):
+            call(i)
         t0 = time.perf_counter()
-        for i in range(args.steps):
-            check(L.cd_pipeline_dc(devs[i % NL].raw, 1, ptr(xs_c[i % N_X]), tau, None, 1, ptr(yh), None, ptr(ah), None))
+        for i in range(64):
+            call(i)
+        per = (time.perf_counter() - t0) / 64
+        n_e2e = max(args.steps, int(np.ceil(0.2 / max(per, 1e-6))))
+        t0 = time.perf_counter()
+        for i in range(n_e2e):
+            call(i)
         dt = time.perf_counter() - t0
-        e2e = {"value": args.steps / dt, "unit": "tokens/s", "h2d_bytes_per_step": 4 * D,
-               "d2h_bytes_per_step": 4 * D + 4, "timing": "wall clock per synchronous C-ABI call",
+        e2e = {"value": round(n_e2e / dt, 1), "unit": "tokens/s", "h2d_bytes_per_step": 4 * D,
+               "d2h_bytes_per_step": 4 * D + 4, "calls": n_e2e,
+               "timing": "wall clock over back-to-back synchronous C-ABI calls (>= 0.2 s, handles warmed)",
                "api": "cd_pipeline_dc (host buffers)"}
 
     # ---- all-reduce share (TP)
     comm = None
     if world > 1:
-        ms_local, gl = graph_rate(torch, step_fn(cd._capi.METHOD_DC, tau, comm=False), args.steps, stream)
-        del gl
-        ms_local = max_over_ranks(ms_local)
-        comm = {"layer_us": 1e3 * ms / args.steps, "compute_only_us": 1e3 * ms_local / args.steps,
-                "allreduce_share": max(0.0, 1 - ms_local / ms), "allreduce_bytes": 4 * D}
+        ms_local, _, _ = timer.run(step_fn(cd._capi.METHOD_DC, tau, comm=False), args.steps)
+        comm = {"layer_us": 1e3 * ms_step, "compute_only_us": 1e3 * ms_local,
+                "allreduce_share": max(0.0, 1 - ms_local / ms_step), "allreduce_bytes": 4 * D}
 
     # ---- sparsity sweep (DC 50/70/80/90, MC 70/90, dense 0%)
     sweep = []
     if not args.no_sweep:
-        n_sw = min(args.steps, 256)
+        n_sw = max(2 * NL, min(args.steps, 64))
         cases = [("dc", k) for k in (0.5, 0.7, 0.8, 0.9)] + [("mc", 0.7), ("mc", 0.9), ("dense", 0.0)]
         u_cal = u_x = None
         for method, k in cases:
             if method == "mc" and u_cal is None:
-                u_cal = np.abs(cd.pipeline_mc(layer, xcal, float("inf"),
-                                              cd.BlockConfig(reduction=cd.Reduction.DeterministicOrdered),
-                                              want_u=True).u)
-                u_x = np.abs(cd.pipeline_mc(layer, xs, float("inf"),
-                                            cd.BlockConfig(reduction=cd.Reduction.DeterministicOrdered),
-                                            want_u=True).u)
+                ordc = cd.BlockConfig(reduction=cd.Reduction.DeterministicOrdered)
+                u_cal = np.abs(cd.pipeline_mc(layer, xcal, float("inf"), ordc, want_u=True).u)
+                u_x = np.abs(cd.pipeline_mc(layer, xs, float("inf"), ordc, want_u=True).u)
             if method == "dc":
                 t = tau_dc(k)
                 al = (z_x[:, rb:re_] > np.float32(t)).sum(axis=1)
                 alf = (z_x > np.float32(t)).sum(axis=1)
                 mid = cd._capi.METHOD_DC
             elif method == "mc":
-                m = m_of(k)
-                t = float(np.mean([row[np.lexsort((np.arange(F), -row))[m]] for row in u_cal]))
+                t = top_m_tau(u_cal, m_of(k))
                 al = (u_x[:, rb:re_] > np.float32(t)).sum(axis=1)
                 alf = (u_x > np.float32(t)).sum(axis=1)
                 mid = cd._capi.METHOD_MC
@@ -490,26 +670,29 @@ def run_ours(args):
                 t, al, alf, mid = 0.0, np.full(N_X, Fl), np.full(N_X, F), cd._capi.METHOD_DENSE
             f = step_fn(mid, t)
             with torch.cuda.stream(stream):
-                for i in range(4):
+                for i in range(2 * NL):
                     f(i, stream.cuda_stream)
-            barrier()
-            ms_k, gk = graph_rate(torch, f, n_sw, stream)
-            del gk
-            ms_k = max_over_ranks(ms_k)
-            us = 1e3 * ms_k / n_sw
+            timer.barrier()
+            ms_k, nt, _ = timer.run(f, n_sw)
+            us = 1e3 * ms_k
             b = float(np.mean([chain_bytes(method, a) for a in al]))
             sweep.append({"method": method, "k": k, "realized_sparsity": round(1 - float(alf.mean()) / F, 4),
                           "tokens_per_s": round(1e3 / us * 1e3, 1), "us_per_token": round(us, 3),
                           "touched_mb_per_rank": round(b / 1e6, 2), "gbs_per_rank": round(b / us / 1e3, 1),
-                          "hbm_frac": round(b / us / 1e3 / peak, 4)})
+                          "hbm_frac": round(b / us / 1e3 / peak, 4), "timed_steps": nt})
         dense = [s for s in sweep if s["method"] == "dense"]
         dc90 = [s for s in sweep if s["method"] == "dc" and s["k"] == 0.9]
         if dense and dc90:
             sweep.append({"speedup_dc90_vs_dense": round(dense[0]["us_per_token"] / dc90[0]["us_per_token"], 2)})
+    del tps, devs
+    layer.invalidate()
 
-    batched = None
+    extra = {}
+    if world == 1 and not args.no_configs:
+        extra["gemma"] = gemma_section(torch, cd, timer, min(args.steps, 64), peak)
+        extra["f32"] = f32_section(torch, cd, timer, min(args.steps, 64), peak, args.k)
     if world == 1 and not args.no_batched:
-        batched = batched_section(torch, cd, stream, min(args.steps, 50), peak)
+        extra["batched"] = batched_section(torch, cd, timer, min(args.steps, 50), peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -518,7 +701,7 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (reference bench() seeded RNG, seed 42; bf16-rounded)",
             "config": {"workload": f"BASELINE configs[1]: llama3.1-8b FFN layer d={D} d_ff={F} SiLU, D-CountDown "
@@ -528,20 +711,22 @@ def run_ours(args):
                        "l2": f"inputs larger than L2: {NL} layer replicas rotated per step "
                              f"({NL * bytes_step / 1e6:.0f} MB touched per rotation > 126 MB L2)",
                        "graph": f"{args.steps} steps in one CUDA graph ({launches_per_step} kernel(s) per step, "
-                                "PDL-chained" + (", + NCCL all-reduce" if world > 1 else "") + ")"},
+                                "PDL-chained" + (", + NCCL all-reduce" if world > 1 else "") +
+                                f"), replayed {reps}x back to back in the timed region ({n_timed} timed steps)"},
+            "timed_steps": n_timed,
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 1), "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": ncu_traffic(names[dom]), "alg_bytes_per_launch": stage_bytes[dom],
+                         "traffic": ncu_traffic(names[dom]), "alg_bytes_per_launch": alg,
                          "launch_us": round(launch_ns / 1e3, 3), "timing": roof_how, "stages": stages,
-                         "step": {"alg_bytes": bytes_step, "gbs": round(bytes_step / (1e6 * ms / args.steps), 1),
-                                  "frac": round(bytes_step / (1e6 * ms / args.steps) / peak, 4)}},
+                         "peak_nominal_gbs": 8000.0, "frac_of_nominal": round(achieved / 8000.0, 4)},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches_per_step * n_timed,
             "clocks": clk.summary(),
+            "flips": flips,
             "sweep": sweep,
-            "batched": batched,
         }
+        line.update(extra)
         if comm:
             line["allreduce"] = comm
         print(json.dumps(line))

@@ -44,42 +44,65 @@ struct SplitMix {
     float normal_f(float mean, float sd) { return mean + sd * static_cast<float>(normal()); }
 };
 
+// splitmix64 is counter-based (numerics.hpp:33-45): the k-th output of Rng(seed) is
+// mix(seed + k * golden), so any stretch of the stream can be generated independently.  The
+// Box-Muller pairs of a fresh stream are (draws 2p+1, 2p+2) -> normals (2p, 2p+1) (cos, then
+// the cached sin), which lets the layer fill run on all host threads, bit-identical to the
+// sequential generator.
+uint64_t splitmix_at(uint64_t seed, uint64_t k) {
+    uint64_t z = seed + k * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+inline double uniform_of(uint64_t u) { return static_cast<double>(u >> 11) * 0x1.0p-53; }
+
 }  // namespace
 
 extern "C" {
 
 // bench() setup sequence; any output may be NULL (its draws are still consumed so the stream
 // position matches the reference).  d_rank <= 0 skips the predictor.
-int cd_synth_layer(uint64_t seed, int64_t d_model,
-                                                          int64_t d_inter, int64_t d_rank,
-                                                          float* w_up, float* w_gate,
-                                                          float* w_down, float* x,
-                                                          float* theta_a, float* theta_b) {
+int cd_synth_layer(uint64_t seed, int64_t d_model, int64_t d_inter, int64_t d_rank, float* w_up,
+                   float* w_gate, float* w_down, float* x, float* theta_a, float* theta_b) {
     if (d_model <= 0 || d_inter <= 0) return CD_ERR_DATA;
-    SplitMix rng(seed);
     const float sd = 1.0f / std::sqrt(static_cast<float>(d_model));
     const int64_t n = d_model * d_inter;
-    float* mats[3] = {w_up, w_gate, w_down};
-    for (float* m : mats)
-        for (int64_t i = 0; i < n; ++i) {
-            const float v = rng.normal_f(0.0f, sd);
-            if (m) m[i] = v;
+    // normals 0 .. 3n-1 fill W_up, W_gate, W_down (sd), then d_model normals of x (sd 1)
+    const int64_t total = 3 * n + d_model;
+    auto store = [&](int64_t k, double v) {
+        if (k < 3 * n) {
+            float* m = k < n ? w_up : (k < 2 * n ? w_gate : w_down);
+            if (m) m[k % n] = 0.0f + sd * static_cast<float>(v);
+        } else if (k < total && x) {
+            x[k - 3 * n] = 0.0f + 1.0f * static_cast<float>(v);
         }
-    for (int64_t i = 0; i < d_model; ++i) {
-        const float v = rng.normal_f(0.0f, 1.0f);
-        if (x) x[i] = v;
+    };
+    const int64_t pairs = (total + 1) / 2;
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < pairs; ++p) {
+        const double u1 = 1.0 - uniform_of(splitmix_at(seed, 2 * static_cast<uint64_t>(p) + 1));
+        const double u2 = uniform_of(splitmix_at(seed, 2 * static_cast<uint64_t>(p) + 2));
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double a = 6.283185307179586476925286766559 * u2;
+        store(2 * p, r * std::cos(a));
+        store(2 * p + 1, r * std::sin(a));
     }
     if (d_rank > 0) {
-        SplitMix prng(rng.next());  // Rng::fork()
+        // Rng::fork(): the next draw after the 2 * pairs Box-Muller draws seeds the child
+        const uint64_t child = splitmix_at(seed, 2 * static_cast<uint64_t>(pairs) + 1);
         const float ba = 1.0f / std::sqrt(static_cast<float>(d_model));
-        for (int64_t i = 0; i < d_model * d_rank; ++i) {
-            const float v = ba * static_cast<float>(2.0 * prng.uniform() - 1.0);
-            if (theta_a) theta_a[i] = v;
-        }
         const float bb = 1.0f / std::sqrt(static_cast<float>(d_rank));
-        for (int64_t i = 0; i < d_rank * d_inter; ++i) {
-            const float v = bb * static_cast<float>(2.0 * prng.uniform() - 1.0);
-            if (theta_b) theta_b[i] = v;
+        const int64_t na = d_model * d_rank, nbm = d_rank * d_inter;
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < na + nbm; ++i) {
+            const double u = uniform_of(splitmix_at(child, static_cast<uint64_t>(i) + 1));
+            if (i < na) {
+                if (theta_a) theta_a[i] = ba * static_cast<float>(2.0 * u - 1.0);
+            } else if (theta_b) {
+                theta_b[i - na] = bb * static_cast<float>(2.0 * u - 1.0);
+            }
         }
     }
     return CD_OK;

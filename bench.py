@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-batched", action="store_true", help="skip BASELINE configs[4] (batch-64 + prefill)")
     p.add_argument("--no-configs", action="store_true", help="skip configs[2] (Gemma) and the f32 line")
+    p.add_argument("--no-stack", action="store_true", help="skip configs[3] (the 32-layer stack)")
     return p.parse_args()
 
 
@@ -516,6 +517,53 @@ def f32_section(torch, cd, timer, steps, peak_gbs, k):
     return out
 
 
+def stack_section(torch, cd, timer, world, rank, steps, peak_gbs, k, n_layers=32):
+    """BASELINE.json configs[3]: the 32-layer Llama-3.1-8B FFN stack, layer l = seed 42 + l,
+    layer l+1's input = RMSNorm(y_l) (fused into k_dc_fused), D-CountDown at k (tau_D
+    calibrated per layer), bf16, d_ff tensor-parallel over the ranks with one NCCL all-reduce
+    per layer; a token's whole stack (32 kernels + 32 all-reduces) is captured in the graph.
+    Reports tokens/s through the stack and the all-reduce's share of layer time."""
+    from paper_2505_17701_b200 import costmodel as cm
+    from paper_2505_17701_b200.tp import TPStack
+    t0 = time.time()
+    st = TPStack.synthetic(n_layers, D, F, R, k, world, rank, seed0=SEED, device=torch.cuda.current_device())
+    build_s = time.time() - t0
+    xs = torch.from_numpy(np.stack([cd.synth_normals(90_000 + i, D) for i in range(4)])).cuda()
+    ys = torch.zeros((n_layers, D), device="cuda")
+    alive = torch.zeros((n_layers, 1), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    with torch.cuda.stream(timer.stream):
+        for i in range(2):
+            st.forward(xs[i % 4], ys, timer.stream.cuda_stream, alive_out=alive)
+    torch.cuda.synchronize()
+    al = alive.cpu().numpy()[:, 0]
+    Fl = st.rows[1] - st.rows[0]
+    bytes_tok = float(sum(cm.device_bytes("dc", D, Fl, R, int(a), 2)["total_bytes"] for a in al))
+
+    def tok(i, cs, comm=True):
+        st.forward(xs[i % 4], ys, cs, comm=comm)
+
+    n = max(2, min(steps, 8))
+    ms, n_timed, _ = timer.run(tok, n)
+    out = {"workload": f"BASELINE configs[3]: {n_layers}-layer llama3.1-8b FFN stack (seeds 42+l), input of layer "
+                       f"l+1 = RMSNorm(y_l) fused into k_dc_fused, D-CountDown r={R} k={k} (tau_D per layer), bf16, "
+                       f"tp{world} over d_ff" + (" + NCCL all-reduce per layer" if world > 1 else ""),
+           "tokens_per_s": round(1e3 / ms, 1), "us_per_token": round(1e3 * ms, 2),
+           "us_per_layer": round(1e3 * ms / n_layers, 3), "timed_tokens": n_timed,
+           "realized_sparsity_rank_layers": round(1 - float(al.mean()) / Fl, 4),
+           "roofline": {"bound": "hbm", "alg_bytes_per_token_per_rank": bytes_tok,
+                        "achieved": round(bytes_tok / ms / 1e6, 1), "peak": peak_gbs, "unit": "GB/s",
+                        "frac": round(bytes_tok / ms / 1e6 / peak_gbs, 4)},
+           "build_s": round(build_s, 1)}
+    if world > 1:
+        ms_c, _, _ = timer.run(lambda i, cs: tok(i, cs, comm=False), n)
+        out["allreduce"] = {"compute_only_us_per_layer": round(1e3 * ms_c / n_layers, 3),
+                            "allreduce_share": round(max(0.0, 1 - ms_c / ms), 4),
+                            "allreduce_bytes": 4 * D, "note": "share = 1 - (stack without the all-reduces) / stack"}
+    del st
+    return out
+
+
 def run_ours(args):
     import torch
     import paper_2505_17701_b200 as cd
@@ -693,6 +741,8 @@ def run_ours(args):
         extra["f32"] = f32_section(torch, cd, timer, min(args.steps, 64), peak, args.k)
     if world == 1 and not args.no_batched:
         extra["batched"] = batched_section(torch, cd, timer, min(args.steps, 50), peak)
+    if not args.no_stack:
+        extra["stack"] = stack_section(torch, cd, timer, world, rank, args.steps, peak, args.k)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

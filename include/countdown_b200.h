@@ -198,6 +198,17 @@ CD_API int cd_forward_device(cd_layer* h, int method, int64_t batch, const float
                       int reduction, const uint8_t* d_mask_override, float* d_y,
                       uint8_t* d_mask, float* d_indicator, int32_t* d_alive, void* stream);
 
+/* cd_forward_device on RMSNorm(d_x): each sample's input is x / sqrt(mean(x^2) + rms_eps)
+ * (no gain).  This is the chaining of configs[3]'s layer stack (layer l+1's
+ * input is the RMS-normalised y_l; the reference has no residual), so a decode step of a
+ * stack is one call per layer on the previous layer's (all-reduced) output with no separate
+ * norm kernel: k_dc_fused normalises inside the step; the other engines run one norm kernel
+ * first.  rms_eps must be finite and >= 0 (CD_ERR_DATA otherwise). */
+CD_API int cd_forward_device_normed(cd_layer* h, int method, int64_t batch, const float* d_x,
+                                    float rms_eps, float tau, int reduction,
+                                    const uint8_t* d_mask_override, float* d_y, uint8_t* d_mask,
+                                    float* d_indicator, int32_t* d_alive, void* stream);
+
 /* Block until all work queued on the handle's stream has finished. */
 CD_API int cd_layer_sync(cd_layer* h);
 

@@ -502,3 +502,12 @@ class Reference:
 
 def reference_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+def rms_norm(y, eps=1e-5):
+    """Input norm of the stacked layers (layer l+1's input is the
+    RMS-normalised y_l, no gain, no residual): y / sqrt(mean(y^2) + eps), in double, rounded
+    once to f32.  Test infrastructure: the product computes it on the device."""
+    y = np.asarray(y, np.float64)
+    return (y / np.sqrt(np.mean(y * y) + eps)).astype(np.float32)
+

@@ -361,8 +361,14 @@ class DeviceLayer:
     def forward_device(self, method: int, x_dev, y_dev, tau: float = 0.0,
                        reduction: int = Reduction.UnorderedAccumulate, batch: int = 1,
                        mask_override=None, mask_out=None, indicator_out=None, alive_out=None,
-                       stream=None) -> None:
+                       stream=None, rms_eps: float | None = None) -> None:
+        """cd_forward_device (rms_eps=None) or cd_forward_device_normed (input = RMSNorm(x))."""
         s = None if stream is None else C.c_void_p(stream)
+        if rms_eps is not None:
+            check(lib().cd_forward_device_normed(self.raw, int(method), int(batch), ptr(x_dev), float(rms_eps),
+                                                 float(tau), int(reduction), ptr(mask_override), ptr(y_dev),
+                                                 ptr(mask_out), ptr(indicator_out), ptr(alive_out), s))
+            return
         check(lib().cd_forward_device(self.raw, int(method), int(batch), ptr(x_dev), float(tau),
                                       int(reduction), ptr(mask_override), ptr(y_dev), ptr(mask_out),
                                       ptr(indicator_out), ptr(alive_out), s))

@@ -109,6 +109,7 @@ struct cd_layer {
     bool weights_finite = true;  // every uploaded weight finite: the row-union GEMM may read any row
     cublasHandle_t blas = nullptr;
     Grow tc_ws, blas_ws;    // tensor-core path workspace; cuBLAS workspace (graph-capture safe)
+    Grow rms_ws;            // RMS-normalised inputs for the engines that do not fuse the norm
     // host-call CUDA graph: [H2D inputs, kernels, D2H outputs] replayed while the call signature
     // (method, batch, tau, options) repeats -- one launch instead of four API calls per step
     struct HostGraph {
@@ -244,6 +245,7 @@ struct Req {
     uint8_t* mask_out = nullptr;
     float* ind_out = nullptr;
     int* alive_out = nullptr;
+    float rms_eps = -1.0f;  // >= 0: the input is RMSNorm(x) (stacked layers)
     cudaStream_t stream = nullptr;
     // Stage timing (cd_bench_stages): PDL off, an event recorded after every launch.
     cudaEvent_t* marks = nullptr;
@@ -297,7 +299,16 @@ int run_chain(cd_layer* h, const Req& r) {
         fail(CD_ERR_DATA, "pipeline_dc: layer has no low-rank predictor attached");
     if (!L.w_up) fail(CD_ERR_DATA, "forward: handle holds only a predictor (no layer weights)");
 
+    // input RMS norm: fused into k_dc_fused where that kernel runs, else one norm kernel first
+    float* xn = r.rms_eps >= 0.0f ? h->rms_ws.get<float>(static_cast<size_t>(r.nb) * d) : nullptr;
     if (tc_eligible(h, r)) {
+        if (xn) {
+            ck(cdk::launch_rmsnorm(r.x, r.nb, d, r.rms_eps, xn, c), "rmsnorm");
+            Req rn = r;
+            rn.x = xn;
+            rn.rms_eps = -1.0f;
+            return 1 + run_chain(h, rn);
+        }
         const cdk::tc::Plan p = cdk::tc::plan_for(r.nb, r.method);
         void* ws = h->tc_ws.get<uint8_t>(cdk::tc::workspace_bytes(L, p, c.num_sms));
         const uint8_t* ovr = r.with_masks ? r.masks_in : r.ovr;
@@ -313,11 +324,19 @@ int run_chain(cd_layer* h, const Req& r) {
         for (int c0 = 0; c0 < r.nb; c0 += kMaxBatchFast) {
             const int n = std::min(kMaxBatchFast, r.nb - c0);
             const float* xc = r.x + c0 * d;
+            auto norm_x = [&]() {
+                if (xn && xc != xn + c0 * d) {
+                    ck(cdk::launch_rmsnorm(r.x + c0 * d, n, d, r.rms_eps, xn + c0 * d, c), "rmsnorm");
+                    xc = xn + c0 * d;
+                    launches += 1;
+                }
+            };
             float* yc = r.y + c0 * d;
             uint8_t* mo = r.mask_out ? r.mask_out + c0 * F : nullptr;
             float* io = r.ind_out ? r.ind_out + c0 * F : nullptr;
             int* ao = r.alive_out ? r.alive_out + c0 : nullptr;
             if (r.with_masks) {
+                norm_x();
                 ck(cdk::launch_compact_masks(L, S, r.masks_in + c0 * F,
                                              r.method != cdk::kDC ? r.u_in + c0 * F : nullptr, n, yc, c),
                    "compact_masks");
@@ -325,15 +344,17 @@ int run_chain(cd_layer* h, const Req& r) {
                 launches += 2;
             } else if (r.method == cdk::kDense) {
                 // two launches: the y-zeroing kernel, then the all-rows FFN kernel
+                norm_x();
                 ck(cdk::launch_sparse_fast(L, S, cdk::kDC, true, xc, n, yc, ao, c), "dense");
                 launches += 2;
                 mark(0);
-            } else if (r.method == cdk::kMC && n == 1 && h->use_fused &&
+            } else if (r.method == cdk::kMC && n == 1 && h->use_fused && (norm_x(), true) &&
                        cdk::launch_mc_fused(L, S, xc, r.tau, yc, mo, io, ao, c) == cudaSuccess) {
                 launches += 1;
                 mark(0);
             } else if (r.method == cdk::kMC || r.method == cdk::kCATS) {
                 (void)cudaGetLastError();
+                norm_x();
                 const bool cats = r.method == cdk::kCATS;
                 ck(cdk::launch_indicator_mc_fast(L, S, xc, n, r.tau, yc, mo, io, c, cats), "indicator_mc");
                 mark(0);
@@ -342,11 +363,12 @@ int run_chain(cd_layer* h, const Req& r) {
                 launches += 2;
             } else if (h->use_fused &&
                        cdk::launch_dc_fused(L, S, xc, n, r.tau, r.ovr ? r.ovr + c0 * F : nullptr, yc, mo, io, ao,
-                                            c) == cudaSuccess) {
+                                            c, r.rms_eps) == cudaSuccess) {
                 launches += 1;
                 mark(0);
             } else {
                 (void)cudaGetLastError();  // an unsupported fused shape: use the chain
+                norm_x();
                 ck(cdk::launch_latent_fast(L, S, xc, n, c), "latent");
                 mark(0);
                 ck(cdk::launch_indicator_dc_fast(L, S, n, r.tau, r.ovr ? r.ovr + c0 * F : nullptr, yc, mo, io, c),
@@ -364,6 +386,11 @@ int run_chain(cd_layer* h, const Req& r) {
     for (int c0 = 0; c0 < r.nb; c0 += kMaxBatch) {
         const int n = std::min(kMaxBatch, r.nb - c0);
         const float* xc = r.x + c0 * d;
+        if (xn) {
+            ck(cdk::launch_rmsnorm(xc, n, d, r.rms_eps, xn + c0 * d, c), "rmsnorm");
+            xc = xn + c0 * d;
+            launches += 1;
+        }
         float* yc = r.y + c0 * d;
         uint8_t* mo = r.mask_out ? r.mask_out + c0 * F : nullptr;
         int* ao = r.alive_out ? r.alive_out + c0 : nullptr;
@@ -711,7 +738,7 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     std::lock_guard<std::recursive_mutex> dlock(ctx.mu);
     h->stream = ctx.stream;
     h->dev_mu = &ctx.mu;
-    for (Grow* g : {&h->tc_ws, &h->blas_ws, &h->g_dx, &h->g_dy, &h->g_dmask_in, &h->g_dmask_out, &h->g_du_in,
+    for (Grow* g : {&h->tc_ws, &h->blas_ws, &h->rms_ws, &h->g_dx, &h->g_dy, &h->g_dmask_in, &h->g_dmask_out, &h->g_du_in,
                     &h->g_dind, &h->g_dalive, &h->g_hx, &h->g_hy, &h->g_hmask, &h->g_hind, &h->g_halive})
         g->gen = &h->gen;
     cdk::LayerDev& L = h->L;
@@ -1178,6 +1205,36 @@ int cd_forward_device(cd_layer* h, int method, int64_t batch, const float* d_x, 
         r.mask_out = d_mask;
         r.ind_out = d_indicator;
         r.alive_out = d_alive;
+        r.stream = static_cast<cudaStream_t>(stream);
+        h->last_launches = run_chain(h, r);
+    });
+}
+
+int cd_forward_device_normed(cd_layer* h, int method, int64_t batch, const float* d_x, float rms_eps, float tau,
+                             int reduction, const uint8_t* d_mask_override, float* d_y, uint8_t* d_mask,
+                             float* d_indicator, int32_t* d_alive, void* stream) {
+    return guarded([&] {
+        check_common(h, batch, d_x, d_y);
+        check_reduction(reduction);
+        if (!(rms_eps >= 0.0f) || !std::isfinite(rms_eps)) fail(CD_ERR_DATA, "rms_eps must be finite and >= 0");
+        if (method != CD_METHOD_DENSE && method != CD_METHOD_MC && method != CD_METHOD_DC &&
+            method != CD_METHOD_CATS)
+            fail(CD_ERR_DATA, "unknown method");
+        if (d_mask_override && method != CD_METHOD_DC) fail(CD_ERR_DATA, "mask override is DC-only");
+        CallLock lk(h);
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        Req r;
+        r.method = method;
+        r.nb = static_cast<int>(batch);
+        r.x = d_x;
+        r.tau = tau;
+        r.reduction = reduction;
+        r.ovr = d_mask_override;
+        r.y = d_y;
+        r.mask_out = d_mask;
+        r.ind_out = d_indicator;
+        r.alive_out = d_alive;
+        r.rms_eps = rms_eps;
         r.stream = static_cast<cudaStream_t>(stream);
         h->last_launches = run_chain(h, r);
     });

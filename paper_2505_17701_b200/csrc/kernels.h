@@ -98,13 +98,16 @@ cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, 
 // uses the three-kernel chain).
 cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
                             const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
-                            int* alive_out, const LaunchCfg& c);
+                            int* alive_out, const LaunchCfg& c, float rms_eps = -1.0f);
 // M-CountDown step (batch 1) as one persistent kernel (kernels_fused_mc.cu): dense u = W_up x
 // over each CTA's neuron chunk, |u| > tau, compaction, and the sparse gate / down stage with
 // the work-stealing schedule.  Zeroes and accumulates y; optional mask / u / alive outputs.
 // Returns cudaErrorInvalidValue for shapes it does not cover (the caller uses the chain).
 cudaError_t launch_mc_fused(const LayerDev& L, const Scratch& S, const float* x, float tau, float* y,
                             uint8_t* mask_out, float* u_out, int* alive_out, const LaunchCfg& c);
+// xn[b] = x[b] / sqrt(mean(x[b]^2) + eps) for b < nb (rows of d values, ld apart): the input
+// RMS norm of stacked layers for the engines that do not fuse it.
+cudaError_t launch_rmsnorm(const float* x, int nb, int64_t d, float eps, float* xn, const LaunchCfg& c);
 // Host-supplied masks (exec_mc / exec_dc): ordered compaction + zero y (+ MC u gather).
 cudaError_t launch_compact_masks(const LayerDev& L, const Scratch& S, const uint8_t* masks,
                                  const float* u_full, int nb, float* y, const LaunchCfg& c);

@@ -769,7 +769,33 @@ __global__ void k_count_nonfinite(const float* __restrict__ v, int64_t n, int* _
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(out, bad);
 }
 
+// Input RMS norm of stacked layers: one CTA per sample, f32 sum of squares (tree order).
+__global__ void k_rmsnorm(const float* __restrict__ x, int64_t d, float eps, float* __restrict__ xn) {
+    __shared__ float part[32];
+    const float* xb = x + blockIdx.x * d;
+    float* ob = xn + blockIdx.x * d;
+    pdl_wait();
+    float ss = 0.0f;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(xb[i], xb[i], ss);
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) part[0] = rsqrtf(v / static_cast<float>(d) + eps);
+    }
+    __syncthreads();
+    pdl_launch_dependents();
+    const float inv = part[0];
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) ob[i] = xb[i] * inv;
+}
+
 // ---------------------------------------------------------------- public launchers
+cudaError_t launch_rmsnorm(const float* x, int nb, int64_t d, float eps, float* xn, const LaunchCfg& c) {
+    return launch_ex(k_rmsnorm, dim3(nb), dim3(512), 0, c, true, x, d, eps, xn);
+}
+
 cudaError_t launch_count_nonfinite(const float* v, int64_t n, int* out, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = (n + 255) / 256;

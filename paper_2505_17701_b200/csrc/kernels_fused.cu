@@ -65,6 +65,7 @@ struct FusedParams {
     float* logits_out;
     int* alive_out;
     float tau;
+    float rms_eps;  // >= 0: the layer's input is RMSNorm(x) = x / sqrt(mean(x^2) + eps) per sample
     int nb, nstages, rows_per_cta, qrows;
     int b_smem;  // bf16: predictor rows staged by TMA in the ring, moved to registers after stage 1
 };
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
     float* red = reinterpret_cast<float*>(own_bits + rows_per_cta);  // [nwc][32] warp partials
     float* sval = red + nwc * 32;                                      // [kGroupF * NB]
     int* cnt = reinterpret_cast<int*>(sval + kGroupF * NB);  // [0] n_own [1..NB] alive [NB+1] tag [NB+2] cap
+    float* rms_red = reinterpret_cast<float*>(cnt + NB + 4);   // [nwc][NB] sum-of-squares partials
 
     const int64_t c0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t c1 = imin64(L.F, c0 + rows_per_cta);
@@ -281,6 +283,31 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
             if (blockIdx.x == 0) {
                 unsigned* nq = S.ctl + kCtlQueue + ((t + 1u) % 3u) * 32u;
                 nq[0] = 0u; nq[1] = 0u; nq[2] = 0u; nq[3] = 0u;
+            }
+        }
+        if (P.rms_eps >= 0.0f) {
+            // input RMS norm (stacked layers): every CTA holds all of x,
+            // so each reduces the sum of squares itself -- one barrier, no exchange
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                float ss = 0.0f;
+#pragma unroll
+                for (int j = 0; j < VPT; ++j)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) ss = fmaf(xr[b][j][k], xr[b][j][k], ss);
+                ss = warp_sum(ss);
+                if (lane == 0) rms_red[warp * NB + b] = ss;
+            }
+            named_bar_sync(kBarC, nc);
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                float ss = 0.0f;
+                for (int w = 0; w < nwc; ++w) ss += rms_red[w * NB + b];
+                const float inv = rsqrtf(ss / static_cast<float>(L.d) + P.rms_eps);
+#pragma unroll
+                for (int j = 0; j < VPT; ++j)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) xr[b][j][k] *= inv;
             }
         }
         if (blockIdx.x == G - 1) {
@@ -715,7 +742,7 @@ cudaError_t read_timeline_fused(unsigned long long*, int64_t) { return cudaError
 
 cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
                             const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
-                            int* alive_out, const LaunchCfg& c) {
+                            int* alive_out, const LaunchCfg& c, float rms_eps) {
     if (!L.theta_at || !S.t_lat || !S.t_list || !S.t_count || !S.t_alive || !S.ctl) return cudaErrorInvalidValue;
     if (c.num_sms >= kYZeroWord || L.F >= (1 << 27)) return cudaErrorInvalidValue;
     // x rows are staged by the TMA engine: 16-byte aligned rows of a multiple of 16 bytes
@@ -744,7 +771,7 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     // (the theta_at slice is overlaid on the ring's tail)
     const int64_t aux_bytes = (int64_t)qrows * L.ld * esz;
     const int64_t fixed = (int64_t)nbk * L.ldr * 4 + 3 * 8 + (int64_t)rpc * 8 + (nwc * 32 + kGroupF * nbk) * 4 +
-                          (3 + nbk) * 4 + 64;
+                          (4 + nbk) * 4 + nwc * nbk * 4 + 64;
     const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
     const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
     if (nstages < 2) return cudaErrorInvalidValue;
@@ -767,6 +794,7 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
         p.logits_out = logits_out;
         p.alive_out = alive_out;
         p.tau = tau;
+        p.rms_eps = rms_eps;
         p.nb = nb;
         p.nstages = nstages;
         p.rows_per_cta = rpc;

@@ -19,8 +19,11 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _capi
 from ._capi import DataError
 from .api import DeviceLayer, GatedMlpLayer, Predictor, Reduction
+
+RMS_EPS = 1e-5  # the stack's input-norm epsilon (Llama-3.1's rms_norm_eps)
 
 
 def shard_range(d_inter: int, world: int, rank: int) -> tuple[int, int]:
@@ -71,6 +74,80 @@ class TPLayer:
         """Partial FFN on the shard, then the sum all-reduce: y_dev holds the full output."""
         self.forward_local(method, x_dev, y_dev, tau, stream, batch, alive_out)
         allreduce_sum_(y_dev, self.group)
+
+
+def stack_step(n_layers: int, x, ys, run_layer, allreduce) -> None:
+    """One decode step through a layer stack (BASELINE.json configs[3]):
+    layer 0 reads x; layer l+1 reads RMSNorm(y_l) -- the reference has no residual, so the
+    stack is the layers chained through an input norm -- and every layer's partial output is
+    summed over the ranks by one all-reduce before the next layer reads it.
+
+    run_layer(l, x_in, y_out, normed) computes layer l's partial output on this rank's neurons
+    into y_out, normalising x_in first when `normed`; allreduce(y) sums y over the ranks in
+    place.  ys[l] keeps every layer's output (layer l+1's input)."""
+    for l in range(n_layers):
+        run_layer(l, x if l == 0 else ys[l - 1], ys[l], l > 0)
+        allreduce(ys[l])
+
+
+class TPStack:
+    """A stack of d_ff-sharded layers on this rank's GPU (configs[3]).  Each layer is a
+    TPLayer (its neuron slice + theta_b rows; theta_a replicated) with its own calibrated
+    threshold; the step is one kernel per layer -- k_dc_fused normalises its input itself
+    (cd_forward_device_normed) -- plus one NCCL all-reduce per layer, all on one stream, so the
+    whole step is capturable in one CUDA graph."""
+
+    def __init__(self, tps: "list[TPLayer]", taus, eps: float = RMS_EPS, group=None,
+                 method: int = _capi.METHOD_DC):
+        if not tps or len(tps) != len(taus):
+            raise DataError("TPStack: need one threshold per layer")
+        self.tps = list(tps)
+        self.taus = [float(t) for t in taus]
+        self.eps, self.group, self.method = float(eps), group, method
+        self.rows = self.tps[0].rows
+
+    @staticmethod
+    def synthetic(n_layers: int, d_model: int, d_inter: int, d_rank: int, k: float, world: int, rank: int,
+                  seed0: int = 42, device: int = 0, device_dtype: str = "bf16", eps: float = RMS_EPS,
+                  group=None, n_cal: int = 8, keep_host: bool = False) -> "TPStack":
+        """configs[3]'s stack: layer l is the reference bench()'s seeded layer + low-rank
+        predictor for seed seed0 + l; tau_D of layer l is calibrated on
+        n_cal N(0, 1) inputs (unit-RMS, like the normalised inputs of layers >= 1) as the mean
+        of the per-input exact top-m logit thresholds (calibration.cpp:11-37 on the logits).
+        Host weights are dropped after each upload unless keep_host."""
+        from .api import calibrate, synth_normals, synth_workload, SparsityMethod
+        tps, taus, host = [], [], []
+        xcal = np.stack([synth_normals(70_000 + i, d_model) for i in range(n_cal)])
+        for l in range(n_layers):
+            layer, _, pred = synth_workload(seed0 + l, d_model, d_inter, d_rank, device_dtype=device_dtype,
+                                            device=device)
+            taus.append(calibrate(layer, xcal, k, SparsityMethod.DCountdown, pred))
+            tps.append(TPLayer(layer, pred, world, rank, device, device_dtype, group))
+            layer.invalidate()
+            if keep_host:
+                host.append((layer, pred))
+        st = TPStack(tps, taus, eps, group)
+        st.host = host
+        return st
+
+    def __len__(self) -> int:
+        return len(self.tps)
+
+    def forward(self, x_dev, ys_dev, stream: int, batch: int = 1, comm: bool = True, masks_out=None,
+                alive_out=None) -> None:
+        """ys_dev[l] <- layer l's (all-reduced) output; ys_dev[-1] is the stack's output.
+        masks_out[l] / alive_out[l] (optional device buffers): layer l's shard-local mask and
+        alive count."""
+
+        def run_layer(l, x_in, y_out, normed):
+            self.tps[l].dev.forward_device(
+                self.method, x_in, y_out, self.taus[l], Reduction.UnorderedAccumulate, batch,
+                mask_out=None if masks_out is None else masks_out[l],
+                alive_out=None if alive_out is None else alive_out[l], stream=stream,
+                rms_eps=self.eps if normed else None)
+
+        stack_step(len(self.tps), x_dev, ys_dev, run_layer,
+                   (lambda y: allreduce_sum_(y, self.group)) if comm else (lambda y: None))
 
 
 def shard_partials_reference(partial_fn, d_inter: int, world: int) -> np.ndarray:

@@ -16,7 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2505_17701_b200 import DataError
-from paper_2505_17701_b200.tp import allreduce_sum_, shard_partials_reference, shard_range
+from paper_2505_17701_b200.tp import allreduce_sum_, shard_partials_reference, shard_range, stack_step, RMS_EPS
 
 
 def test_shard_range_partitions():
@@ -104,3 +104,63 @@ def test_shard_partials_reference_sums_in_rank_order(oracle):
     for G in (1, 2, 4, 8):
         y = shard_partials_reference(part, 40, G)
         assert np.linalg.norm(y - full) <= 1e-5 * np.linalg.norm(full)
+
+
+def _stack_worker(rank, world, port, q):
+    """configs[3] host logic: a 2-layer stack, each rank thresholding and computing its own
+    neuron slice of every layer, the product's stack_step chaining the layers through the input
+    RMS norm and one all-reduce per layer."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle as O
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = O.Oracle()
+        d, F, r, L = 48, 200, 8, 2
+        gs = [o.generate(42 + l, d, F, r) for l in range(L)]
+        taus = [float(np.quantile(o.lowrank_logits(g["theta_a"], g["theta_b"], g["x"])[1], 0.7)) for g in gs]
+        b, e = shard_range(F, world, rank)
+        x = torch.from_numpy(gs[0]["x"].copy())
+        ys = [torch.zeros(d) for _ in range(L)]
+        alive = [0] * L
+
+        def run_layer(l, x_in, y_out, normed):
+            g = gs[l]
+            xi = O.rms_norm(x_in.numpy(), RMS_EPS) if normed else x_in.numpy()
+            _, z = o.lowrank_logits(g["theta_a"], g["theta_b"], xi)
+            m = (z[b:e] > np.float32(taus[l])).astype(np.uint8)
+            alive[l] = int(m.sum())
+            shard = {k: g[k][b:e] for k in ("w_up", "w_gate", "w_down")}
+            y_out.copy_(torch.from_numpy(o.forward_sparse(shard, xi, m).copy()))
+
+        stack_step(L, x, ys, run_layer, allreduce_sum_)
+        # single device: the same stack without sharding
+        xi = gs[0]["x"]
+        for l in range(L):
+            if l > 0:
+                xi = O.rms_norm(y, RMS_EPS)
+            _, z = o.lowrank_logits(gs[l]["theta_a"], gs[l]["theta_b"], xi)
+            y = o.forward_sparse(gs[l], xi, (z > np.float32(taus[l])).astype(np.uint8))
+        err = float(np.linalg.norm(ys[-1].numpy().astype(np.float64) - y) / np.linalg.norm(y))
+        q.put((rank, err, alive))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp_two_layer_stack_matches_single_device():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stack_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    for _, err, alive in res:
+        assert err <= 1e-5
+        assert all(a > 0 for a in alive)

@@ -219,6 +219,14 @@ CD_API int cd_predictor_create(int device, int64_t d_model, int64_t d_rank, int6
                                int dtype, const float* theta_a, const float* theta_b,
                                cd_layer** out);
 
+/* Ternary predictor handle (TernaryPredictor, predictor.hpp:23-34): q is the d_model x d_inter
+ * quantized view (TernaryPredictor::quantized(), codes -1 / 0 / 1) and gamma its scale
+ * (gamma()).  cd_predict_logits on it computes z = x @ (gamma * Q) with the reference's fold
+ * (predictor.cpp:116-126), bit-identical.  Exact kernels only: the decode hot path is the
+ * low-rank predictor. */
+CD_API int cd_predictor_create_ternary(int device, int64_t d_model, int64_t d_inter, float gamma,
+                                       const int8_t* q, cd_layer** out);
+
 /* ---------------------------------------------------------------- timing
  * bench() (blocked_exec.hpp:85-86) device analogue: upload x (batch x d_model, host) once, run
  * `warmup` untimed forwards, then `iters` forwards each bracketed by CUDA events on the

@@ -68,6 +68,7 @@ _SIGNATURES = {
     "cd_layer_sync": [_vp],
     "cd_layer_set_engines": [_vp, _i32],
     "cd_predictor_create": [_i32, _i64, _i64, _i64, _i32, _vp, _vp, _vp],
+    "cd_predictor_create_ternary": [_i32, _i64, _i64, _f32, _vp, _vp],
     "cd_bench_device": [_vp, _i32, _i64, _vp, _f32, _i32, _i64, _i64, _vp],
     "cd_bench_stages": [_vp, _i32, _i32, _i64, _vp, _f32, _i64, _i64, _vp, _vp],
     "cd_synth_layer": [_u64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp],

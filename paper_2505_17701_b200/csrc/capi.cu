@@ -977,6 +977,7 @@ int cd_layer_set_predictor(cd_layer* h, int64_t d_rank, const float* theta_a, co
         if (h->hg.exec) cudaGraphExecDestroy(h->hg.exec);
         h->hg = {};
         ++h->gen;
+        L.pred_kind = 0;
         L.r = d_rank;
         L.ldr = ldr;
         L.theta_a = ta;
@@ -1170,6 +1171,20 @@ int cd_predict_logits(cd_layer* h, int64_t batch, const float* x, float* logits)
             const int n = static_cast<int>(std::min<int64_t>(kMaxBatch, batch - c0));
             std::memcpy(h->h_x, x + c0 * L.d, sizeof(float) * n * L.d);
             ck(cudaMemcpyAsync(h->d_x, h->h_x, sizeof(float) * n * L.d, cudaMemcpyHostToDevice, h->stream), "H2D");
+            if (L.pred_kind == 1) {
+                // ternary: z[j] = fold_i (x[i] * gamma) * q[i][j] (predictor.cpp:116-126) -- the
+                // same ascending fold as the low-rank second stage, with Q^T as theta_bt
+                float* xs = h->S.ex_lat;
+                for (int b = 0; b < n; ++b)
+                    ck(cdk::launch_exact_scale(h->d_x + b * L.d, L.d, L.gamma, xs + b * L.ldr, c), "scale");
+                ck(cdk::launch_exact_rowdot_all(L.theta_bt, L.dtype, L.F, L.ldr, L.d, xs, L.ldr, n, h->d_ind, L.F, c),
+                   "ternary logits");
+                ck(cudaMemcpyAsync(h->h_ind, h->d_ind, sizeof(float) * n * L.F, cudaMemcpyDeviceToHost, h->stream),
+                   "D2H");
+                ck(cudaStreamSynchronize(h->stream), "predict_logits");
+                std::memcpy(logits + c0 * L.F, h->h_ind, sizeof(float) * n * L.F);
+                continue;
+            }
             ck(cdk::launch_exact_latent(L, h->S, h->d_x, n, c), "latent");
             ck(cdk::launch_exact_rowdot_all(L.theta_bt, L.dtype, L.F, L.ldr, L.r, h->S.ex_lat, L.ldr, n, h->d_ind,
                                             L.F, c),
@@ -1248,6 +1263,41 @@ int cd_predictor_create(int device, int64_t d_model, int64_t d_rank, int64_t d_i
                                                 nullptr, nullptr, nullptr, true));
         const int rc = cd_layer_set_predictor(h.get(), d_rank, theta_a, theta_b);
         if (rc != CD_OK) throw Fail{rc};
+        *out = h.release();
+    });
+}
+
+int cd_predictor_create_ternary(int device, int64_t d_model, int64_t d_inter, float gamma, const int8_t* q,
+                                cd_layer** out) {
+    return guarded([&] {
+        if (!out || !q) fail(CD_ERR_DATA, "predictor: null argument");
+        if (d_model <= 0 || d_inter <= 0) fail(CD_ERR_DATA, "make_ternary_predictor: dims must be positive");
+        if (!std::isfinite(gamma)) fail(CD_ERR_DATA, "ternary predictor: non-finite scale");
+        std::unique_ptr<cd_layer> h(create_impl(device, d_model, d_inter, 0, d_inter, CD_ACT_SILU, CD_DTYPE_F32,
+                                                nullptr, nullptr, nullptr, true));
+        CallLock lk(h.get());
+        cdk::LayerDev& L = h->L;
+        const int64_t ldr = round_up(d_model, cdk::kVecElems);
+        std::vector<float> qf(static_cast<size_t>(d_model * d_inter));
+        for (size_t i = 0; i < qf.size(); ++i) {
+            if (q[i] < -1 || q[i] > 1) fail(CD_ERR_DATA, "ternary predictor: codes must be -1, 0 or 1");
+            qf[i] = static_cast<float>(q[i]);
+        }
+        void* tbt = h->dalloc<uint8_t>(static_cast<size_t>(d_inter * ldr) * sizeof(float), false);
+        float* tmp = nullptr;
+        ck(cudaMalloc(&tmp, sizeof(float) * qf.size()), "cudaMalloc tmp");
+        cudaError_t e = cudaMemcpyAsync(tmp, qf.data(), sizeof(float) * qf.size(), cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess)
+            e = cdk::launch_pack_transpose(tmp, d_model, d_inter, 0, d_inter, tbt, CD_DTYPE_F32, ldr, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        cudaFree(tmp);
+        ck(e, "ternary predictor upload");
+        h->S.ex_lat = h->dalloc<float>(static_cast<size_t>(kMaxBatch * ldr));
+        L.pred_kind = 1;
+        L.gamma = gamma;
+        L.r = d_model;
+        L.ldr = ldr;
+        L.theta_bt = tbt;
         *out = h.release();
     });
 }

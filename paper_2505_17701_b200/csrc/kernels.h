@@ -38,6 +38,8 @@ struct LayerDev {
     const void* theta_a = nullptr;   // d x ldr
     const void* theta_at = nullptr;  // r x ld  (theta_a transposed: one latent column per row)
     const void* theta_bt = nullptr;  // F x ldr
+    int pred_kind = 0;               // 0: low-rank (theta_a, theta_bt); 1: ternary (Q^T in theta_bt)
+    float gamma = 0.0f;              // ternary scale
 };
 
 // Per-handle device scratch.  latent/count/done are "self-cleaning": every kernel
@@ -132,6 +134,8 @@ cudaError_t launch_exact_phase1(const LayerDev& L, const Scratch& S, int method,
                                 const LaunchCfg& c);
 // v[i] = act(v[i]) in place, double precision / one rounding (numerics.cpp:47-67).
 cudaError_t launch_exact_act(int act, float* v, int64_t n, const LaunchCfg& c);
+// out[i] = x[i] * g (one f32 rounding): the ternary predictor's scaled input.
+cudaError_t launch_exact_scale(const float* x, int64_t n, float g, float* out, const LaunchCfg& c);
 // y[b][j] = fold over list (ascending neuron) of s * W_down[i][j] for alive samples.
 cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,
                               const LaunchCfg& c);

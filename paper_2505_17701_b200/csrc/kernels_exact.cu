@@ -185,6 +185,12 @@ __global__ void ke_act(int act, float* __restrict__ v, int64_t n) {
         v[i] = act_exact(act, v[i]);
 }
 
+// ternary predictor input (predictor.cpp:116-126): out[i] = x[i] * gamma, one f32 rounding.
+__global__ void ke_scale(const float* __restrict__ x, int64_t n, float g, float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __fmul_rn(x[i], g);
+}
+
 // ============================================================================ exact down projection
 // down_projection Ordered (blocked_exec.cpp:85-97) == weighted_sum (gated_mlp.cpp:28-44):
 // y[j] = fold over alive i ascending of s[i] * W_down[i][j]; one thread per column.
@@ -287,6 +293,11 @@ cudaError_t launch_exact_phase1(const LayerDev& L, const Scratch& S, int method,
 cudaError_t launch_exact_act(int act, float* v, int64_t n, const LaunchCfg& c) {
     const int blocks = static_cast<int>(imin64(1024, (n + 255) / 256));
     return launch_ex(ke_act, dim3(blocks), dim3(256), 0, c, false, act, v, n);
+}
+
+cudaError_t launch_exact_scale(const float* x, int64_t n, float g, float* out, const LaunchCfg& c) {
+    const int blocks = static_cast<int>(imin64(1024, (n + 255) / 256));
+    return launch_ex(ke_scale, dim3(blocks), dim3(256), 0, c, false, x, n, g, out);
 }
 
 cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,

@@ -32,135 +32,14 @@
 
 #include "countdown/blocked_exec.hpp"
 #include "countdown_b200.h"
+#include "gpu_handles.hpp"
 
 namespace countdown {
 
+using gpu_shim::cache;
+using gpu_shim::raise_rc;
+
 namespace {
-
-void raise_rc(int rc) {
-    if (rc == CD_OK) return;
-    const std::string msg = cd_last_error();
-    if (rc == CD_ERR_DATA) throw DataError(msg);
-    if (rc == CD_ERR_NUMERIC) throw NumericError(msg);
-    throw std::runtime_error("countdown_b200: " + msg);
-}
-
-// Content hash of a weight matrix: EVERY element, so an in-place edit of a cached layer's
-// weights is always seen (the reference API has no invalidate call).  Four independent
-// multiply-xorshift lanes over 64-bit words per 1 MiB chunk, chunks hashed in parallel
-// (OpenMP, as the reference's own build) and combined in order: ~30 GB/s on 16 cores, i.e.
-// ~25 ms for the 700 MB Llama-shape layer.
-inline uint64_t mix64(uint64_t h) {
-    h ^= h >> 33;
-    h *= 0xff51afd7ed558ccdull;
-    h ^= h >> 33;
-    h *= 0xc4ceb9fe1a85ec53ull;
-    h ^= h >> 33;
-    return h;
-}
-
-uint64_t chunk_hash(const uint64_t* w, size_t n, uint64_t seed) {
-    uint64_t a = seed ^ 0x9E3779B97F4A7C15ull, b = seed + 0x632BE59BD9B4E019ull, c = ~seed, d = seed * 3;
-    size_t i = 0;
-    for (; i + 4 <= n; i += 4) {
-        a = (a ^ w[i]) * 0x9FB21C651E98DF25ull;
-        b = (b ^ w[i + 1]) * 0x9FB21C651E98DF25ull;
-        c = (c ^ w[i + 2]) * 0x9FB21C651E98DF25ull;
-        d = (d ^ w[i + 3]) * 0x9FB21C651E98DF25ull;
-        a ^= a >> 29;
-        b ^= b >> 29;
-        c ^= c >> 29;
-        d ^= d >> 29;
-    }
-    for (; i < n; ++i) a = mix64(a ^ w[i]);
-    return mix64(a ^ mix64(b ^ mix64(c ^ mix64(d))));
-}
-
-uint64_t content_hash(const std::vector<float>& v, uint64_t h = 0xcbf29ce484222325ull) {
-    const size_t n = v.size();
-    const size_t words = n / 2;
-    const uint64_t* w = reinterpret_cast<const uint64_t*>(v.data());  // std::vector storage: 8-aligned
-    constexpr size_t kChunk = size_t(1) << 17;                        // words (1 MiB)
-    const int64_t nchunks = static_cast<int64_t>((words + kChunk - 1) / kChunk);
-    std::vector<uint64_t> part(static_cast<size_t>(nchunks));
-#pragma omp parallel for schedule(static) if (nchunks > 8)
-    for (int64_t c = 0; c < nchunks; ++c) {
-        const size_t b = static_cast<size_t>(c) * kChunk;
-        part[static_cast<size_t>(c)] = chunk_hash(w + b, std::min(kChunk, words - b), static_cast<uint64_t>(c));
-    }
-    for (uint64_t p : part) h = mix64(h ^ p);
-    if (n & 1) {
-        uint32_t u;
-        std::memcpy(&u, &v[n - 1], 4);
-        h = mix64(h ^ u);
-    }
-    return mix64(h ^ n);
-}
-
-struct Entry {
-    const float *up, *gate, *down;
-    int64_t d, F;
-    Activation act;
-    uint64_t hash;
-    cd_layer* h;
-    const float *ta, *tb;
-    int64_t r;
-    uint64_t phash;
-};
-
-class HandleCache {
-  public:
-    ~HandleCache() {
-        for (auto& e : entries_) cd_layer_destroy(e.h);
-    }
-
-    cd_layer* get(const GatedMlpLayer& L, const Predictor* p) {
-        std::lock_guard<std::mutex> g(mu_);
-        const uint64_t hash = content_hash(L.w_down.data, content_hash(L.w_gate.data, content_hash(L.w_up.data)));
-        auto it = std::find_if(entries_.begin(), entries_.end(), [&](const Entry& e) {
-            return e.up == L.w_up.data.data() && e.gate == L.w_gate.data.data() && e.down == L.w_down.data.data() &&
-                   e.d == L.d_model && e.F == L.d_inter && e.act == L.activation && e.hash == hash;
-        });
-        if (it == entries_.end()) {
-            cd_layer* h = nullptr;
-            raise_rc(cd_layer_create(0, L.d_model, L.d_inter, L.activation == Activation::Silu ? CD_ACT_SILU : CD_ACT_GELU_TANH,
-                                     CD_DTYPE_F32, L.w_up.data.data(), L.w_gate.data.data(), L.w_down.data.data(), &h));
-            entries_.push_front(Entry{L.w_up.data.data(), L.w_gate.data.data(), L.w_down.data.data(), L.d_model,
-                                      L.d_inter, L.activation, hash, h, nullptr, nullptr, 0, 0});
-            if (entries_.size() > kCap) {
-                cd_layer_destroy(entries_.back().h);
-                entries_.pop_back();
-            }
-            it = entries_.begin();
-        } else if (it != entries_.begin()) {
-            entries_.splice(entries_.begin(), entries_, it);
-            it = entries_.begin();
-        }
-        if (p) {
-            const LowRankPredictor& lp = p->lowrank();
-            const uint64_t ph = content_hash(lp.theta_b.data, content_hash(lp.theta_a.data));
-            if (it->ta != lp.theta_a.data.data() || it->tb != lp.theta_b.data.data() || it->r != lp.d_rank ||
-                it->phash != ph) {
-                raise_rc(cd_layer_set_predictor(it->h, lp.d_rank, lp.theta_a.data.data(), lp.theta_b.data.data()));
-                it->ta = lp.theta_a.data.data();
-                it->tb = lp.theta_b.data.data();
-                it->r = lp.d_rank;
-                it->phash = ph;
-            }
-        }
-        return it->h;
-    }
-
-  private:
-    static constexpr size_t kCap = 8;
-    std::mutex mu_;
-    std::list<Entry> entries_;
-};
-
-HandleCache& cache() {
-    static HandleCache c;
-    return c;
-}
 
 int red_of(const BlockConfig& cfg) {
     return cfg.reduction == Reduction::DeterministicOrdered ? CD_REDUCTION_ORDERED : CD_REDUCTION_UNORDERED;

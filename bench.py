@@ -351,10 +351,15 @@ def exact_logits(cd, pred, xs):
 
 
 def top_m_tau(rows, m):
-    """Mean over samples of each sample's exact top-m threshold (calibration.cpp:11-37:
-    the (m+1)-th largest value, ties to the lower index, numerics.cpp:105-142)."""
-    n = rows.shape[1]
-    return float(np.mean([row[np.lexsort((np.arange(n), -row))[m]] if m < n else -np.inf for row in rows]))
+    """Mean over samples of each sample's exact top-m threshold (calibration.cpp:11-37: the
+    (m+1)-th largest value, ties to the lower index, numerics.cpp:105-142), selected on the
+    device (cd_top_m, signed order: the rows are logits or |u|), mean in double in order."""
+    import paper_2505_17701_b200 as cd
+    taus, _ = cd.top_m_threshold(np.atleast_2d(rows), m, signed=True)
+    acc = 0.0
+    for t in taus:
+        acc += float(t)
+    return acc / len(taus)
 
 
 def flip_report(torch, cd, dev, method, xs, tau, z_exact, band=1e-6):

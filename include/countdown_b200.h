@@ -227,6 +227,28 @@ CD_API int cd_predictor_create(int device, int64_t d_model, int64_t d_rank, int6
 CD_API int cd_predictor_create_ternary(int device, int64_t d_model, int64_t d_inter, float gamma,
                                        const int8_t* q, cd_layer** out);
 
+/* ---------------------------------------------------------------- selection / calibration
+ * top_m_threshold (numerics.hpp:96-100, numerics.cpp:105-142) for `batch` vectors of n values
+ * (host buffers): the m lanes of largest magnitude, ties to the lower index; tau_out[b] = the
+ * (m+1)-th magnitude (+inf for m = 0, -inf for m = n); mask_out (batch x n, optional) = those
+ * lanes.  signed_order != 0 orders by the value itself instead of |value| (the D-CountDown
+ * tau_D calibration).  Errors as the reference: n = 0 or m outside [0, n] -> CD_ERR_DATA. */
+CD_API int cd_top_m(int device, int64_t batch, int64_t n, const float* v, int64_t m, int signed_order,
+                    float* tau_out, uint8_t* mask_out);
+/* The same on device buffers (rows ld apart; mask rows n apart), asynchronous on `stream`. */
+CD_API int cd_top_m_device(const float* d_v, int64_t batch, int64_t n, int64_t ld, int64_t m,
+                           int signed_order, float* d_tau, uint8_t* d_mask, void* stream);
+
+/* calibrate (calibration.hpp:20-21, calibration.cpp:11-37) on the device: for each of the
+ * n_samples inputs xs (host, n_samples x d_model) the exact indicator -- u = W_up x for
+ * CD_METHOD_MC, h = act(W_gate x) for CD_METHOD_CATS -- and its exact top-m threshold
+ * (m = alive_count_for(k, d_inter)); *tau_hat = their mean in double, ascending sample order.
+ * Bit-identical to the reference.  per_sample (optional): the n_samples thresholds.
+ * CD_METHOD_DC (no reference equivalent: the reference rejects dc here) calibrates tau_D on the
+ * signed predictor logits (Alg. 3) the same way. */
+CD_API int cd_calibrate(cd_layer* h, int method, int64_t n_samples, const float* xs, double k,
+                        double* tau_hat, float* per_sample);
+
 /* ---------------------------------------------------------------- timing
  * bench() (blocked_exec.hpp:85-86) device analogue: upload x (batch x d_model, host) once, run
  * `warmup` untimed forwards, then `iters` forwards each bracketed by CUDA events on the

@@ -681,34 +681,41 @@ def forward_practical(layer: GatedMlpLayer, x, cfg: SparsityConfig, ctx: Practic
     return PracticalResult(r.y, r.mask)
 
 
+def top_m_threshold(v, m: int, signed: bool = False, device: int = 0):
+    """top_m_threshold (numerics.cpp:105-142) on the device (cd_top_m): the m lanes of largest
+    magnitude (ties to the lower index) and tau = the (m+1)-th magnitude (+inf for m = 0, -inf
+    for m = n).  A batch (B x n) gives B results.  signed=True orders by the value itself.
+    Returns (tau, mask) -- arrays for a batch."""
+    v = np.ascontiguousarray(v, np.float32)
+    single = v.ndim == 1
+    vb = np.atleast_2d(v)
+    B, n = vb.shape
+    tau = np.empty(B, np.float32)
+    mask = np.empty((B, n), np.uint8)
+    check(lib().cd_top_m(device, B, n, ptr(vb), int(m), 1 if signed else 0, ptr(tau), ptr(mask)))
+    return (float(tau[0]), mask[0]) if single else (tau, mask)
+
+
 def calibrate(layer: GatedMlpLayer, xs, k: float, method: SparsityMethod,
-              predictor: Predictor | None = None) -> float:
-    """calibrate (calibration.cpp:11-37) on the device: tau = mean over the T samples of each
-    sample's exact top-m threshold, m = alive_count_for(k, d_inter), accumulated in double
-    in sample order.  MC thresholds |u| (u = W_up x, the exact kernels: bitwise the
-    reference's gemv); DC extends it to the predictor logits s_hat (signed, Alg. 3's tau_D,
-    PAPER.md:645), for which the reference has no calibrator (predict_mask fixes 0)."""
+              predictor: Predictor | None = None, per_sample: bool = False):
+    """calibrate (calibration.cpp:11-37) on the device (cd_calibrate): tau = mean over the T
+    samples of each sample's exact top-m threshold, m = alive_count_for(k, d_inter), accumulated
+    in double in sample order.  MC thresholds |u| (u = W_up x), CATS |act(W_gate x)| -- the
+    exact kernels, bitwise the reference's.  DC extends it to the predictor logits s_hat
+    (signed, Alg. 3's tau_D), for which the reference has no calibrator
+    (predict_mask fixes 0).  per_sample=True also returns the T per-sample thresholds."""
     xb, _ = _batched(xs, layer.d_model, "calibrate")
     if xb.shape[0] == 0:
-        raise DataError("calibrate: need at least one sample")
-    m = alive_count_for(k, layer.d_inter)
-    if method == SparsityMethod.MCountdown:
-        ind = np.abs(pipeline_mc(layer, xb, float("inf"), BlockConfig(reduction=Reduction.DeterministicOrdered),
-                                 want_u=True).u)
-    elif method == SparsityMethod.DCountdown:
-        if predictor is None:
-            raise DataError("calibrate: dc needs a predictor")
-        ind = np.atleast_2d(predict_logits(predictor, xb))
-    else:
-        raise DataError("calibrate: cats is not part of the B200 hot path")
-    ind = np.atleast_2d(ind)
-    F = layer.d_inter
-    acc = 0.0
-    for row in ind:
-        # top_m_threshold (numerics.cpp:105-142): the (m+1)-th largest value, ties -> lower index
-        order = np.lexsort((np.arange(F), -row))
-        acc += float(row[order[m]]) if m < F else float("-inf")
-    return acc / ind.shape[0]
+        raise DataError("calibrate: no calibration samples")
+    mid = {SparsityMethod.MCountdown: _capi.METHOD_MC, SparsityMethod.Cats: _capi.METHOD_CATS,
+           SparsityMethod.DCountdown: _capi.METHOD_DC}[SparsityMethod(method)]
+    if mid == _capi.METHOD_DC and predictor is None:
+        raise DataError("calibrate: dc needs a predictor")
+    dev = layer.device_layer(predictor if mid == _capi.METHOD_DC else None)
+    tau = C.c_double()
+    taus = np.empty(xb.shape[0], np.float32)
+    check(lib().cd_calibrate(dev.raw, mid, xb.shape[0], ptr(xb), float(k), C.byref(tau), ptr(taus)))
+    return (float(tau.value), taus) if per_sample else float(tau.value)
 
 
 def realized_sparsity(mask: ActivationMask) -> float:
@@ -898,8 +905,7 @@ def bench(method: str, shape: ShapeSpec, k: float, iters: int, cfg: BlockConfig 
             # largest value, so exactly m rows are alive (the reference instead overrides
             # with the ideal top-m |s| mask, blocked_exec.cpp:411,423: same count and bytes).
             ind = predict_logits(pred, x)
-        order = np.lexsort((np.arange(F), -ind))
-        tau = float(ind[order[m]]) if m < F else float("-inf")
+        tau, _ = top_m_threshold(ind, m, signed=(method == "dc"))
     ns = dev.bench_device(_METHOD_IDS[method], x, tau, red, warmup, iters)
     ns = np.sort(ns)
     p = lambda q: int(ns[int(round(q * (len(ns) - 1)))])

@@ -1302,6 +1302,120 @@ int cd_predictor_create_ternary(int device, int64_t d_model, int64_t d_inter, fl
     });
 }
 
+// alive_count_for (sparsity.cpp:19-27), same messages.
+int64_t alive_count(double k, int64_t F) {
+    if (!(k > 0.0 && k < 1.0)) {
+        std::ostringstream oss;
+        oss << "alive_count_for: k = " << k << " outside (0, 1)";
+        fail(CD_ERR_DATA, oss.str());
+    }
+    if (F <= 0) fail(CD_ERR_DATA, "alive_count_for: d_inter must be positive");
+    return static_cast<int64_t>(std::floor((1.0 - k) * static_cast<double>(F)));
+}
+
+int cd_top_m(int device, int64_t batch, int64_t n, const float* v, int64_t m, int signed_order, float* tau_out,
+             uint8_t* mask_out) {
+    return guarded([&] {
+        if (n <= 0) fail(CD_ERR_DATA, "top_m_threshold: empty vector");
+        if (m < 0 || m > n) {
+            std::ostringstream oss;
+            oss << "top_m_threshold: m = " << m << " outside [0, " << n << "]";
+            fail(CD_ERR_DATA, oss.str());
+        }
+        if (batch <= 0 || !v) fail(CD_ERR_DATA, "top_m: bad arguments");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        DeviceCtx& ctx = device_ctx(device);
+        std::lock_guard<std::recursive_mutex> dl(ctx.mu);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const size_t nv = static_cast<size_t>(batch * n);
+        float* dv = nullptr;
+        ck(cudaMalloc(&dv, nv * sizeof(float) + nv + static_cast<size_t>(batch) * sizeof(float) + 16), "cudaMalloc");
+        uint8_t* dm = reinterpret_cast<uint8_t*>(dv + nv);
+        float* dt = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(dm + nv + 15) & ~uintptr_t{15});
+        cdk::LaunchCfg c;
+        c.num_sms = sms;
+        c.stream = ctx.stream;
+        cudaError_t e = cudaMemcpyAsync(dv, v, nv * sizeof(float), cudaMemcpyHostToDevice, c.stream);
+        if (e == cudaSuccess)
+            e = cdk::launch_top_m(dv, static_cast<int>(batch), n, n, m, signed_order != 0, dt, mask_out ? dm : nullptr,
+                                  n, c);
+        if (e == cudaSuccess && tau_out)
+            e = cudaMemcpyAsync(tau_out, dt, static_cast<size_t>(batch) * sizeof(float), cudaMemcpyDeviceToHost, c.stream);
+        if (e == cudaSuccess && mask_out) e = cudaMemcpyAsync(mask_out, dm, nv, cudaMemcpyDeviceToHost, c.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+        cudaFree(dv);
+        ck(e, "top_m");
+    });
+}
+
+int cd_top_m_device(const float* d_v, int64_t batch, int64_t n, int64_t ld, int64_t m, int signed_order,
+                    float* d_tau, uint8_t* d_mask, void* stream) {
+    return guarded([&] {
+        if (n <= 0) fail(CD_ERR_DATA, "top_m_threshold: empty vector");
+        if (m < 0 || m > n) {
+            std::ostringstream oss;
+            oss << "top_m_threshold: m = " << m << " outside [0, " << n << "]";
+            fail(CD_ERR_DATA, oss.str());
+        }
+        if (batch <= 0 || !d_v || ld < n) fail(CD_ERR_DATA, "top_m: bad arguments");
+        cdk::LaunchCfg c;
+        c.stream = static_cast<cudaStream_t>(stream);
+        ck(cdk::launch_top_m(d_v, static_cast<int>(batch), n, ld, m, signed_order != 0, d_tau, d_mask, n, c), "top_m");
+    });
+}
+
+int cd_calibrate(cd_layer* h, int method, int64_t n_samples, const float* xs, double k, double* tau_hat,
+                 float* per_sample) {
+    return guarded([&] {
+        check_layer(h);
+        if (!xs || !tau_hat) fail(CD_ERR_DATA, "calibrate: null argument");
+        if (n_samples <= 0) fail(CD_ERR_DATA, "calibrate: no calibration samples");
+        if (method != CD_METHOD_MC && method != CD_METHOD_CATS && method != CD_METHOD_DC)
+            fail(CD_ERR_DATA, "calibrate: unknown indicator");
+        const cdk::LayerDev& L = h->L;
+        if (method == CD_METHOD_DC ? !L.theta_bt : !L.w_up)
+            fail(CD_ERR_DATA, method == CD_METHOD_DC ? "calibrate: dc needs a predictor attached"
+                                                     : "calibrate: handle holds no layer weights");
+        const int64_t m = alive_count(k, L.F);
+        CallLock lk(h);
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        cdk::LaunchCfg c;
+        c.num_sms = h->num_sms;
+        c.stream = h->stream;
+        std::vector<float> taus(static_cast<size_t>(n_samples));
+        float* d_tau = h->d_ind;  // scratch: kMaxBatch * F >= kMaxBatch
+        for (int64_t c0 = 0; c0 < n_samples; c0 += kMaxBatch) {
+            const int n = static_cast<int>(std::min<int64_t>(kMaxBatch, n_samples - c0));
+            ck(cudaMemcpyAsync(h->d_x, xs + c0 * L.d, sizeof(float) * n * L.d, cudaMemcpyHostToDevice, c.stream), "H2D");
+            // the indicator with the exact kernels (bitwise the reference's gemv / apply_activation /
+            // predict_logits folds): u = W_up x (MC), h = act(W_gate x) (CATS), s_hat (DC)
+            float* ind = h->S.ind;
+            if (method == CD_METHOD_MC) {
+                ck(cdk::launch_exact_rowdot_all(L.w_up, L.dtype, L.F, L.rs, L.d, h->d_x, L.d, n, ind, L.F, c), "u");
+            } else if (method == CD_METHOD_CATS) {
+                ck(cdk::launch_exact_rowdot_all(L.w_gate, L.dtype, L.F, L.rs, L.d, h->d_x, L.d, n, ind, L.F, c), "gate");
+                ck(cdk::launch_exact_act(L.act, ind, static_cast<int64_t>(n) * L.F, c), "act");
+            } else {
+                ck(cdk::launch_exact_latent(L, h->S, h->d_x, n, c), "latent");
+                ck(cdk::launch_exact_rowdot_all(L.theta_bt, L.dtype, L.F, L.ldr, L.r, h->S.ex_lat, L.ldr, n, ind, L.F, c),
+                   "logits");
+            }
+            // MC / CATS: magnitude top-m (calibration.cpp:29-30); DC: the signed logits (Alg. 3's
+            // tau_D thresholds s_hat itself)
+            ck(cdk::launch_top_m(ind, n, L.F, L.F, m, method == CD_METHOD_DC, d_tau, nullptr, 0, c), "top_m");
+            ck(cudaMemcpyAsync(taus.data() + c0, d_tau, sizeof(float) * n, cudaMemcpyDeviceToHost, c.stream), "D2H");
+        }
+        ck(cudaStreamSynchronize(c.stream), "calibrate");
+        // fixed ascending-order mean in double (calibration.cpp:33-36)
+        double sum = 0.0;
+        for (float t : taus) sum += static_cast<double>(t);
+        *tau_hat = sum / static_cast<double>(n_samples);
+        if (per_sample) std::memcpy(per_sample, taus.data(), taus.size() * sizeof(float));
+        h->last_launches = 0;
+    });
+}
+
 int cd_bench_device(cd_layer* h, int method, int64_t batch, const float* x, float tau, int reduction,
                     int64_t warmup, int64_t iters, int64_t* ns_out) {
     return guarded([&] {

@@ -140,6 +140,13 @@ cudaError_t launch_exact_scale(const float* x, int64_t n, float g, float* out, c
 cudaError_t launch_exact_down(const LayerDev& L, const Scratch& S, int nb, float* y,
                               const LaunchCfg& c);
 
+// Exact top-m per sample (top_m_threshold, numerics.cpp:105-142): rows of n values, ld apart;
+// magnitude order (signed_order false) or signed order; ties to the lower index.  tau_out[b]
+// (optional) = the (m+1)-th value (+inf for m <= 0, -inf for m >= n); mask_out (optional) rows
+// ld_mask apart, the first m lanes in that order alive.
+cudaError_t launch_top_m(const float* v, int batch, int64_t n, int64_t ld, int64_t m, bool signed_order,
+                         float* tau_out, uint8_t* mask_out, int64_t ld_mask, const LaunchCfg& c);
+
 // dst[0, bytes) = src[0, bytes) by a kernel (either side may be mapped pinned host memory).
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, cudaStream_t s);
 

@@ -711,6 +711,18 @@ void check_finite_blob(const float* p, size_t n, const std::string& path, const 
                                   std::to_string(i));
 }
 
+// Sub-allocation of one block: a sizing pass (base null) then a carving pass.
+struct Carve {
+    size_t off = 0;
+    uint8_t* base = nullptr;
+    template <typename T> T* take(size_t n) {
+        off = (off + 255) & ~size_t{255};
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += std::max<size_t>(n, 1) * sizeof(T);
+        return p;
+    }
+};
+
 cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_t re, int act,
                       int dtype, const float* w_up, const float* w_gate, const float* w_down,
                       bool predictor_only = false) {
@@ -784,32 +796,50 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     }
 
     cdk::Scratch& S = h->S;
-    S.list = h->dalloc<int32_t>(L.F);
-    S.bits = h->dalloc<uint32_t>(L.F);
-    S.list_val = h->dalloc<float>(L.F * kMaxBatchFast);
-    S.count = h->dalloc<int>(1);
-    S.done = h->dalloc<int>(1);
-    S.alive = h->dalloc<int>(kMaxBatch);
-    S.ctl = h->dalloc<unsigned>(128);
-    S.t_list = h->dalloc<unsigned long long>(L.F);
-    S.t_aux = h->dalloc<unsigned long long>(L.F);
-    S.t_count = h->dalloc<unsigned long long>(cdk::kMaxCtas);
-    S.t_alive = h->dalloc<unsigned long long>(cdk::kMaxCtas * kMaxBatchFast);
-    S.tc_flags = h->dalloc<unsigned>(cdk::kMaxCtas + 64);
-    S.ind = h->dalloc<float>(kMaxBatch * L.F);
-    S.ex_s = h->dalloc<float>(kMaxBatch * L.F);
-    h->d_x = h->dalloc<float>(kMaxBatch * d);
-    h->d_y = h->dalloc<float>(kMaxBatch * d);
-    h->d_mask_in = h->dalloc<uint8_t>(kMaxBatch * L.F);
-    h->d_mask_out = h->dalloc<uint8_t>(kMaxBatch * L.F);
-    h->d_u_in = h->dalloc<float>(kMaxBatch * L.F);
-    h->d_ind = h->dalloc<float>(kMaxBatch * L.F);
-    h->d_alive = h->dalloc<int>(kMaxBatch);
-    h->h_x = h->halloc<float>(kMaxBatch * d);
-    h->h_y = h->halloc<float>(kMaxBatch * d);
-    h->h_mask = h->halloc<uint8_t>(kMaxBatch * L.F);
-    h->h_ind = h->halloc<float>(kMaxBatch * L.F);
-    h->h_alive = h->halloc<int>(kMaxBatch);
+    // scratch and staging: ONE zeroed device block and ONE mapped pinned block, carved up
+    // (a handle is created per cached layer by the C++ shims: ~20 separate allocations cost
+    // more than the small layers' calls themselves)
+    const size_t Fz = static_cast<size_t>(L.F), dz = static_cast<size_t>(d);
+    auto carve_dev = [&](Carve& cv) {
+        S.list = cv.take<int32_t>(Fz);
+        S.bits = cv.take<uint32_t>(Fz);
+        S.list_val = cv.take<float>(Fz * kMaxBatchFast);
+        S.count = cv.take<int>(1);
+        S.done = cv.take<int>(1);
+        S.alive = cv.take<int>(kMaxBatch);
+        S.ctl = cv.take<unsigned>(128);
+        S.t_list = cv.take<unsigned long long>(Fz);
+        S.t_aux = cv.take<unsigned long long>(Fz);
+        S.t_count = cv.take<unsigned long long>(cdk::kMaxCtas);
+        S.t_alive = cv.take<unsigned long long>(cdk::kMaxCtas * kMaxBatchFast);
+        S.tc_flags = cv.take<unsigned>(cdk::kMaxCtas + 64);
+        S.ind = cv.take<float>(kMaxBatch * Fz);
+        S.ex_s = cv.take<float>(kMaxBatch * Fz);
+        h->d_x = cv.take<float>(kMaxBatch * dz);
+        h->d_y = cv.take<float>(kMaxBatch * dz);
+        h->d_mask_in = cv.take<uint8_t>(kMaxBatch * Fz);
+        h->d_mask_out = cv.take<uint8_t>(kMaxBatch * Fz);
+        h->d_u_in = cv.take<float>(kMaxBatch * Fz);
+        h->d_ind = cv.take<float>(kMaxBatch * Fz);
+        h->d_alive = cv.take<int>(kMaxBatch);
+    };
+    Carve sizing;
+    carve_dev(sizing);
+    Carve dev_cv;
+    dev_cv.base = h->dalloc<uint8_t>(sizing.off);  // zeroed
+    carve_dev(dev_cv);
+    auto carve_host = [&](Carve& cv) {
+        h->h_x = cv.take<float>(kMaxBatch * dz);
+        h->h_y = cv.take<float>(kMaxBatch * dz);
+        h->h_mask = cv.take<uint8_t>(kMaxBatch * Fz);
+        h->h_ind = cv.take<float>(kMaxBatch * Fz);
+        h->h_alive = cv.take<int>(kMaxBatch);
+    };
+    Carve hsize;
+    carve_host(hsize);
+    Carve host_cv;
+    host_cv.base = h->halloc<uint8_t>(hsize.off);
+    carve_host(host_cv);
     return h.release();
 }
 

@@ -209,6 +209,14 @@ CD_API int cd_forward_device_normed(cd_layer* h, int method, int64_t batch, cons
                                     const uint8_t* d_mask_override, float* d_y, uint8_t* d_mask,
                                     float* d_indicator, int32_t* d_alive, void* stream);
 
+/* Weight prefetch across a sequence of layers (a decode step through a stack, or layers
+ * replayed in a fixed order): every fused D-CountDown step on `h` prefetches the predictor of
+ * `next` (same shape, dtype and rank) into L2 once its own records are issued, so the step that
+ * runs `next` reads its theta from L2 -- the HBM bytes move under this step's record stream,
+ * off the next step's latent -> logits chain.  Weights only: correct whatever runs next.
+ * NULL clears.  Re-issue after cd_layer_set_predictor(next, ...) (the theta buffers move). */
+CD_API int cd_layer_set_prefetch(cd_layer* h, const cd_layer* next);
+
 /* Block until all work queued on the handle's stream has finished. */
 CD_API int cd_layer_sync(cd_layer* h);
 

@@ -66,6 +66,7 @@ _SIGNATURES = {
     "cd_forward_device": [_vp, _i32, _i64, _vp, _f32, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "cd_forward_device_normed": [_vp, _i32, _i64, _vp, _f32, _f32, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "cd_layer_sync": [_vp],
+    "cd_layer_set_prefetch": [_vp, _vp],
     "cd_top_m": [_i32, _i64, _i64, _vp, _i64, _i32, _vp, _vp],
     "cd_top_m_device": [_vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp],
     "cd_calibrate": [_vp, _i32, _i64, _vp, C.c_double, _vp, _vp],

@@ -38,7 +38,7 @@ __all__ = [
     "SparsityMode", "SparsityConfig", "PracticalContext", "PracticalResult", "PipelineResult",
     "BenchStats", "DeviceLayer", "exec_dense", "exec_mc", "exec_cats", "exec_dc", "pipeline_dense",
     "pipeline_mc", "pipeline_cats", "pipeline_dc", "forward_sparse", "forward_practical", "predict_logits",
-    "predict_mask", "calibrate", "realized_sparsity", "bench", "synth_workload", "synth_normals",
+    "predict_mask", "calibrate", "top_m_threshold", "realized_sparsity", "bench", "synth_workload", "synth_normals",
     "DataError", "NumericError", "CudaError", "ModelFile", "read_model", "write_model", "checksum_hex",
 ]
 
@@ -382,6 +382,11 @@ class DeviceLayer:
 
     def sync(self) -> None:
         check(lib().cd_layer_sync(self.raw))
+
+    def set_prefetch(self, nxt: "DeviceLayer | None") -> None:
+        """cd_layer_set_prefetch: each fused D-CountDown step on this layer L2-prefetches the
+        predictor of `nxt` (the layer that runs next; same shape), or nothing for None."""
+        check(lib().cd_layer_set_prefetch(self.raw, None if nxt is None else nxt.raw))
 
     def set_engines(self, fused: bool = True, tensor: bool = True, host_graph: bool = True) -> None:
         """cd_layer_set_engines: pick the engines this handle may use (A/B tests; all on by

@@ -107,6 +107,8 @@ struct cd_layer {
     bool use_fused = true;  // batch <= 4 DC / MC as one persistent kernel (off: the kernel chains)
     bool use_tc = true;     // batches >= kTcMinBatch of a bf16 layer on the tensor cores
     bool weights_finite = true;  // every uploaded weight finite: the row-union GEMM may read any row
+    const void* pf_at = nullptr;  // cd_layer_set_prefetch: the next layer's predictor (L2 prefetch)
+    const void* pf_bt = nullptr;
     cublasHandle_t blas = nullptr;
     Grow tc_ws, blas_ws;    // tensor-core path workspace; cuBLAS workspace (graph-capture safe)
     Grow rms_ws;            // RMS-normalised inputs for the engines that do not fuse the norm
@@ -199,17 +201,22 @@ struct DeviceCtx {
     std::recursive_mutex mu;
 };
 
+// Never destroyed: handles freed during static destruction (a C++ caller's cache, destroyed
+// after this library's statics) must still find their device's lock.
 DeviceCtx& device_ctx(int device) {
-    static std::mutex mu;
-    static std::map<int, std::unique_ptr<DeviceCtx>> ctxs;
-    std::lock_guard<std::mutex> g(mu);
-    auto it = ctxs.find(device);
-    if (it != ctxs.end()) return *it->second;
-    auto c = std::make_unique<DeviceCtx>();
-    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    DeviceCtx& ref = *c;
-    ctxs.emplace(device, std::move(c));
-    return ref;
+    static std::mutex* mu = new std::mutex;
+    static auto* ctxs = new std::map<int, DeviceCtx*>;
+    std::lock_guard<std::mutex> g(*mu);
+    auto it = ctxs->find(device);
+    if (it != ctxs->end()) return *it->second;
+    auto* c = new DeviceCtx;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        ck(cudaGetLastError(), "cudaStreamCreate");
+        fail(CD_ERR_CUDA, "cudaStreamCreate failed");
+    }
+    ctxs->emplace(device, c);
+    return *c;
 }
 
 // Device lock, then handle lock (always in this order).
@@ -363,7 +370,7 @@ int run_chain(cd_layer* h, const Req& r) {
                 launches += 2;
             } else if (h->use_fused &&
                        cdk::launch_dc_fused(L, S, xc, n, r.tau, r.ovr ? r.ovr + c0 * F : nullptr, yc, mo, io, ao,
-                                            c, r.rms_eps) == cudaSuccess) {
+                                            c, r.rms_eps, h->pf_at, h->pf_bt) == cudaSuccess) {
                 launches += 1;
                 mark(0);
             } else {
@@ -1561,6 +1568,21 @@ int cd_layer_set_engines(cd_layer* h, int engines) {
         }
         h->hg = {};
         ++h->gen;
+    });
+}
+
+int cd_layer_set_prefetch(cd_layer* h, const cd_layer* next) {
+    return guarded([&] {
+        check_layer(h);
+        CallLock lk(h);
+        h->pf_at = h->pf_bt = nullptr;
+        if (!next) return;
+        const cdk::LayerDev &a = h->L, &b = next->L;
+        if (next->device != h->device || a.d != b.d || a.F != b.F || a.ld != b.ld || a.dtype != b.dtype ||
+            a.r != b.r || a.ldr != b.ldr || !b.theta_at || !b.theta_bt || b.pred_kind != 0)
+            fail(CD_ERR_DATA, "set_prefetch: the next layer must have the same shape, dtype and a low-rank predictor");
+        h->pf_at = b.theta_at;
+        h->pf_bt = b.theta_bt;
     });
 }
 

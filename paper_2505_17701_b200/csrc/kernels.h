@@ -95,12 +95,14 @@ cudaError_t launch_sparse_fast(const LayerDev& L, const Scratch& S, int method, 
                                const float* x, int nb, float* y, int* alive_out,
                                const LaunchCfg& c);
 // D-CountDown step as one persistent kernel (kernels_fused.cu): latent, predictor, threshold,
+// (pf_at / pf_bt: theta_at / theta_bt of the next layer of identical shape, L2-prefetched),
 // compaction and the sparse FFN (work-stealing schedule); zeroes and accumulates y, writes
 // alive_out.  Returns cudaErrorInvalidValue for shapes it does not cover (the caller then
 // uses the three-kernel chain).
 cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
                             const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
-                            int* alive_out, const LaunchCfg& c, float rms_eps = -1.0f);
+                            int* alive_out, const LaunchCfg& c, float rms_eps = -1.0f,
+                            const void* pf_at = nullptr, const void* pf_bt = nullptr);
 // M-CountDown step (batch 1) as one persistent kernel (kernels_fused_mc.cu): dense u = W_up x
 // over each CTA's neuron chunk, |u| > tau, compaction, and the sparse gate / down stage with
 // the work-stealing schedule.  Zeroes and accumulates y; optional mask / u / alive outputs.

@@ -48,7 +48,9 @@ using namespace fused;
 constexpr int kRBf = 8;       // predictor rows per warp iteration (stage 2)
 constexpr int kGroupF = 4;    // neurons per reduction round (stage 3)
 constexpr int kSmemBudgetF = 220 * 1024;
-constexpr int kMaxConsumers = 512;  // consumer threads per CTA (16 warps) + one producer warp
+// consumer threads per CTA (15 warps) + one producer warp: 16 warps = 512 threads keep the
+// register cap at 128 per thread (17 warps are allocated as 20 and capped at 96 -> spills)
+constexpr int kMaxConsumers = 480;
 struct MetaF {
     int32_t idx;
     uint32_t bits;
@@ -66,12 +68,18 @@ struct FusedParams {
     int* alive_out;
     float tau;
     float rms_eps;  // >= 0: the layer's input is RMSNorm(x) = x / sqrt(mean(x^2) + eps) per sample
+    // the predictor of the layer that runs NEXT on this stream (same shape), or null: each CTA
+    // prefetches its own slices of it into L2 once its records are issued, so the next step's
+    // latent / logits stages read L2 instead of waiting on HBM (weights only: no dependence
+    // on this step's output)
+    const void* pf_at;
+    const void* pf_bt;
     int nb, nstages, rows_per_cta, qrows;
     int b_smem;  // bf16: predictor rows staged by TMA in the ring, moved to registers after stage 1
 };
 
 template <typename W, int NB, int VPT, int VPL>
-__global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ FusedParams P) {
     // bf16 layers keep the CTA's predictor rows in REGISTERS, loaded before griddepcontrol.wait
     // (the stage is then pure FFMA once the latent arrives); f32 layers stage them through smem
     constexpr bool kRegB = std::is_same<W, __nv_bfloat16>::value;
@@ -198,6 +206,15 @@ __global__ void __launch_bounds__(544, 1) k_dc_fused(const __grid_constant__ Fus
             red_add_u32(qc + 2, 1u);  // pushed (stealers check each entry's tag, no ordering needed)
             TL(6, 6);
             for (; e < kept; ++e) issue(own_idx[e], own_bits[e]);
+            if (P.pf_bt) {
+                // the next layer's theta slices of this CTA -> L2 (queued behind the records)
+                if (nq > 0)
+                    bulk_prefetch_l2(static_cast<const W*>(P.pf_at) + (int64_t)q0 * L.ld,
+                                     static_cast<uint32_t>(nq * arow_bytes));
+                for (int64_t off = 0; off < nrows * brow_bytes; off += 32768)
+                    bulk_prefetch_l2(static_cast<const uint8_t*>(P.pf_bt) + c0 * brow_bytes + off,
+                                     static_cast<uint32_t>(imin64(32768, nrows * brow_bytes - off)));
+            }
             // steal: claim queue slots until every CTA has pushed and the claim is past the tail
             const unsigned G_u = static_cast<unsigned>(G);
             for (;;) {
@@ -742,7 +759,8 @@ cudaError_t read_timeline_fused(unsigned long long*, int64_t) { return cudaError
 
 cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x, int nb, float tau,
                             const uint8_t* mask_override, float* y, uint8_t* mask_out, float* logits_out,
-                            int* alive_out, const LaunchCfg& c, float rms_eps) {
+                            int* alive_out, const LaunchCfg& c, float rms_eps, const void* pf_at,
+                            const void* pf_bt) {
     if (!L.theta_at || !S.t_lat || !S.t_list || !S.t_count || !S.t_alive || !S.ctl) return cudaErrorInvalidValue;
     if (c.num_sms >= kYZeroWord || L.F >= (1 << 27)) return cudaErrorInvalidValue;
     // x rows are staged by the TMA engine: 16-byte aligned rows of a multiple of 16 bytes
@@ -765,7 +783,12 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     const int64_t esz = L.dtype == kBF16 ? 2 : 4;
     const int64_t stage_bytes = 3 * L.ld * esz;
     const int64_t brow_bytes = L.ldr * esz;
-    const int nwc = static_cast<int>(std::max<int64_t>(8, ((nvec + vpt - 1) / vpt + kWarp - 1) / kWarp));
+    // consumer warps: enough for the columns at vpt vectors each and (bf16) for the chunk's
+    // predictor rows at 8 per warp; at most 15 (+ the producer warp = 512 threads)
+    int64_t nwc64 = std::max<int64_t>(8, ((nvec + vpt - 1) / vpt + kWarp - 1) / kWarp);
+    if (regb) nwc64 = std::max<int64_t>(nwc64, (rpc + 7) / 8);
+    const int nwc = static_cast<int>(nwc64);
+    if (nwc * kWarp > kMaxConsumers) return cudaErrorInvalidValue;
     const int threads = (nwc + 1) * kWarp;
     // fixed carve-up beside the ring: latent, barriers, meta, lists, scratch, latent fragments
     // (the theta_at slice is overlaid on the ring's tail)
@@ -795,6 +818,8 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
         p.alive_out = alive_out;
         p.tau = tau;
         p.rms_eps = rms_eps;
+        p.pf_at = pf_bt ? pf_at : nullptr;
+        p.pf_bt = pf_at ? pf_bt : nullptr;
         p.nb = nb;
         p.nstages = nstages;
         p.rows_per_cta = rpc;

@@ -103,6 +103,11 @@ class TPStack:
             raise DataError("TPStack: need one threshold per layer")
         self.tps = list(tps)
         self.taus = [float(t) for t in taus]
+        if method == _capi.METHOD_DC:
+            # a step runs the layers in order (then layer 0 of the next step): each layer
+            # L2-prefetches the next one's predictor under its own record stream
+            for l, t in enumerate(self.tps):
+                t.dev.set_prefetch(self.tps[(l + 1) % len(self.tps)].dev)
         self.eps, self.group, self.method = float(eps), group, method
         self.rows = self.tps[0].rows
 

@@ -58,7 +58,8 @@ def parse():
     p.add_argument("--no-batched", action="store_true", help="skip BASELINE configs[4] (batch-64 + prefill)")
     p.add_argument("--no-configs", action="store_true", help="skip configs[2] (Gemma) and the f32 line")
     p.add_argument("--no-stack", action="store_true", help="skip configs[3] (the 32-layer stack)")
-    p.add_argument("--no-prefetch", action="store_true", help="no L2 prefetch of the next layer's predictor")
+    p.add_argument("--prefetch", action="store_true",
+                   help="L2-prefetch the next layer's predictor in each step (measured slower: off by default)")
     return p.parse_args()
 
 
@@ -402,8 +403,6 @@ def gemma_section(torch, cd, timer, steps, peak_gbs):
         layer, _, pred = cd.synth_workload(SEED + 100 + i, Dg, Fg, Rg, activation=cd.Activation.GeluTanh,
                                            device_dtype="bf16")
         layers.append((layer, pred, layer.device_layer(pred)))
-    for i in range(NL):
-        layers[i][2].set_prefetch(layers[(i + 1) % NL][2])
     layer0, pred0, _ = layers[0]
     xcal = np.stack([cd.synth_normals(50_000 + i, Dg) for i in range(16)])
     xs = np.stack([cd.synth_normals(60_000 + i, Dg) for i in range(16)])
@@ -601,7 +600,7 @@ def run_ours(args):
     NL = args.layers
     tps = [TPLayer(layer, pred, world, rank, device=local, device_dtype="bf16") for _ in range(NL)]
     devs = [t.dev for t in tps]
-    if not args.no_prefetch:
+    if args.prefetch:
         # the replicas run in a fixed rotation: each step L2-prefetches the next one's predictor
         for i, dv in enumerate(devs):
             dv.set_prefetch(devs[(i + 1) % NL])

@@ -45,15 +45,43 @@ namespace {
 
 using namespace fused;
 
+#ifndef CD_LAT_REP
+#define CD_LAT_REP 8  // max latent copies (t_lat holds kMaxBatchFast x 2048 words)
+#endif
+#ifndef CD_PF_EARLY
+#define CD_PF_EARLY 1  // next-layer predictor prefetch issued at the start of the chain (0: behind the records)
+#endif
+
 constexpr int kRBf = 8;       // predictor rows per warp iteration (stage 2)
 constexpr int kGroupF = 4;    // neurons per reduction round (stage 3)
 constexpr int kSmemBudgetF = 220 * 1024;
 // consumer threads per CTA (15 warps) + one producer warp: 16 warps = 512 threads keep the
 // register cap at 128 per thread (17 warps are allocated as 20 and capped at 96 -> spills)
 constexpr int kMaxConsumers = 480;
+#ifdef CD_TIMELINE
+// development build: stamps of the last 4 launches, slot = launch tag % 4 (stamps taken before
+// the tag is known are held in registers)
+static __device__ unsigned long long g_tlf[4][kTlKernels][kTlCtas][kTlPhases];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TLF(k, p) do { if (blockIdx.x < kTlCtas) g_tlf[tl_tag & 3u][k][blockIdx.x][p] = gtime(); } while (0)
+#define TLV(k, p, v) do { if (blockIdx.x < kTlCtas) g_tlf[tl_tag & 3u][k][blockIdx.x][p] = (v); } while (0)
+#define TLC(p) do { if (blockIdx.x < kTlCtas) g_tlf[tl_tag & 3u][2][blockIdx.x][p] = clock64(); } while (0)
+#else
+#define TLC(p) ((void)0)
+#define TLF(k, p) ((void)0)
+#define TLV(k, p, v) ((void)0)
+#endif
+
 struct MetaF {
     int32_t idx;
     uint32_t bits;
+    int32_t seq;  // position in the stage sequence (split stage 3: dot warps run n_dot records
+                  // ahead, so a parity wait can alias the stage's previous use -- checked here)
+    int32_t pad;
 };
 
 // Kernel arguments in one block (read through the constant bank as instruction operands).
@@ -76,6 +104,9 @@ struct FusedParams {
     const void* pf_bt;
     int nb, nstages, rows_per_cta, qrows;
     int b_smem;  // bf16: predictor rows staged by TMA in the ring, moved to registers after stage 1
+    int n_dot;   // batch-1 bf16 stage 3: warps computing the records' up/gate dots (the rest: down)
+    int lat_rep; // latent published in lat_rep copies; CTA c gathers copy c % lat_rep (spreads
+                 // the all-CTA read of the same lines over lat_rep x more L2 lines)
 };
 
 template <typename W, int NB, int VPT, int VPL>
@@ -93,10 +124,19 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
     float* __restrict__ y = P.y;
     uint8_t* __restrict__ mask_out = P.mask_out;
     float* __restrict__ logits_out = P.logits_out;
-    if (threadIdx.x == 0) TL(5, 0);
+#ifdef CD_TIMELINE
+    uint32_t tl_tag = 0;
+    unsigned long long tl_h0 = gtime(), tl_h1 = 0, tl_h2 = 0;
+#endif
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int kBarC = 1;   // consumers only
     constexpr int kBarK = 3;   // consumers -> producer: own list, counts and launch tag in smem
+    constexpr int kBarD = 2;   // stage-3 down warps (split stage 3)
+    // batch-1 bf16: stage 3 splits each record between one "dot" warp (u, g over the whole row
+    // from shared memory, s = u act(g)) and the "down" warps (column-owned y += s W_down[i]),
+    // handing s over through a per-stage mbarrier -- no CTA-wide barrier per record group
+    constexpr bool kSplit3 = kRegB && NB == 1;
+    constexpr int kVPD = 4;    // down-warp column vectors per thread (<= 4: d <= 32 x 8 x nd)
     const int nwc = blockDim.x / kWarp - 1;
     const int nc = nwc * kWarp;
     const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
@@ -124,6 +164,11 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
     float* sval = red + nwc * 32;                                      // [kGroupF * NB]
     int* cnt = reinterpret_cast<int*>(sval + kGroupF * NB);  // [0] n_own [1..NB] alive [NB+1] tag [NB+2] cap
     float* rms_red = reinterpret_cast<float*>(cnt + NB + 4);   // [nwc][NB] sum-of-squares partials
+    // split stage 3: per-stage s hand-over barriers and values, x as f32 for the dot warps
+    uint64_t* sready = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(rms_red + nwc * NB) + 15) & ~uintptr_t(15));
+    float* svs = reinterpret_cast<float*>(sready + nstages);
+    float* xs = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(svs + nstages) + 15) & ~uintptr_t(15));
+    const int n_dot = kSplit3 ? P.n_dot : 0;
 
     const int64_t c0 = (int64_t)blockIdx.x * rows_per_cta;
     const int64_t c1 = imin64(L.F, c0 + rows_per_cta);
@@ -135,7 +180,8 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
     if (threadIdx.x == 0) {
         for (int s = 0; s < nstages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], nwc);
+            mbar_init(&empty[s], kSplit3 ? 1 + (nwc - n_dot) : nwc);
+            if (kSplit3) mbar_init(&sready[s], 1);
         }
         mbar_init(bar_a, 1);
         mbar_init(bar_b, 1);
@@ -154,6 +200,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         const uint64_t pol = policy_evict_first();
         int st = 0;
         uint32_t ph = 0;
+        int pseq = 0;
         if (lane == 0) {
             // prologue: weights only (step-independent), overlaps the previous grid's tail
             if (nq > 0) {
@@ -166,29 +213,60 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bytes));
                 bulk_g2s(ring, BT + c0 * brow_bytes, static_cast<uint32_t>(bytes), bar_b, pol);
             }
+#if CD_PF_EARLY
+            if (P.pf_bt) {
+                // the next layer's theta slices of this CTA -> L2 while this step's dependent
+                // chain (x -> latent -> logits -> mask) leaves HBM idle: the next step's prologue
+                // then reads L2 instead of competing with this step's record stream for HBM.
+                // After griddepcontrol.wait, so it does not compete with the previous step's.
+                pdl_wait();
+                if (nq > 0)
+                    bulk_prefetch_l2(static_cast<const W*>(P.pf_at) + (int64_t)q0 * L.ld,
+                                     static_cast<uint32_t>(nq * arow_bytes));
+                for (int64_t off = 0; off < nrows * brow_bytes; off += 32768)
+                    bulk_prefetch_l2(static_cast<const uint8_t*>(P.pf_bt) + c0 * brow_bytes + off,
+                                     static_cast<uint32_t>(imin64(32768, nrows * brow_bytes - off)));
+            }
+#endif
         }
         __syncwarp();
         auto issue = [&](int32_t i, uint32_t bits) {
             mbar_wait(&empty[st], ph ^ 1);
             meta[st].idx = i;
             meta[st].bits = bits;
+            meta[st].seq = pseq++;
             mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rec_bytes));
             bulk_g2s(ring + st * stage_bytes, REC + (int64_t)i * L.rs, static_cast<uint32_t>(rec_bytes), &full[st],
                      pol);
             if (++st == nstages) { st = 0; ph ^= 1; }
         };
+#ifdef CD_TIMELINE
+        if (lane == 0) {  // arrival of the predictor slices (development build only)
+            if (nq > 0) { mbar_wait(bar_a, 0); tl_h1 = gtime(); }
+            if ((!kRegB || P.b_smem) && nrows > 0) { mbar_wait(bar_b, 0); tl_h2 = gtime(); }
+        }
+        __syncwarp();
+#endif
         // ---- stage 3 schedule: this CTA's own active neurons up to the cap, its overflow
         // published to the launch's work queue, then stealing from that queue until empty.
         named_bar_sync(kBarK, nc + kWarp);
         const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
+#ifdef CD_TIMELINE
+        tl_tag = tag;
+        if (lane == 0) {
+            if (tl_h1) TLV(1, 4, tl_h1);
+            if (tl_h2) TLV(1, 5, tl_h2);
+        }
+#endif
         const int n_own = cnt[0];
         const int kept = min(n_own, cnt[NB + 2]);
         const int ovf = n_own - kept;
         unsigned* qc = S.ctl + kCtlQueue + (tag % 3u) * 32u;  // [0] tail [1] head [2] pushed [3] actives
         int e = 0;
         if (lane == 0) {
-            TL(6, 5);
+            TLF(6, 5);
             for (; e < min(kept, nstages); ++e) issue(own_idx[e], own_bits[e]);  // fresh ring: no wait
+            TLF(1, 0);
         }
         int base = 0;
         if (lane == 0) {
@@ -204,9 +282,10 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         __syncwarp();
         if (lane == 0) {
             red_add_u32(qc + 2, 1u);  // pushed (stealers check each entry's tag, no ordering needed)
-            TL(6, 6);
+            TLF(6, 6);
             for (; e < kept; ++e) issue(own_idx[e], own_bits[e]);
-            if (P.pf_bt) {
+            TLF(1, 1);
+            if (!CD_PF_EARLY && P.pf_bt) {
                 // the next layer's theta slices of this CTA -> L2 (queued behind the records)
                 if (nq > 0)
                     bulk_prefetch_l2(static_cast<const W*>(P.pf_at) + (int64_t)q0 * L.ld,
@@ -215,13 +294,19 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                     bulk_prefetch_l2(static_cast<const uint8_t*>(P.pf_bt) + c0 * brow_bytes + off,
                                      static_cast<uint32_t>(imin64(32768, nrows * brow_bytes - off)));
             }
-            // steal: claim queue slots until every CTA has pushed and the claim is past the tail
+            // steal: claim queue slots until the claim is past the final tail (known once every
+            // CTA has pushed).  The next claim is requested before the current record waits for a
+            // ring slot, so the last (empty) claim is usually back by the time the ring drains
+            // and the sentinel follows the last record at once.
             const unsigned G_u = static_cast<unsigned>(G);
+            unsigned tail_final = 0xFFFFFFFFu;
+            int n_stolen = 0;
+            unsigned next = atomicAdd(qc + 1, 1u);
             for (;;) {
-                const unsigned slot = atomicAdd(qc + 1, 1u);
+                const unsigned slot = next;
                 bool got = false;
                 uint32_t wv = 0;
-                for (;;) {
+                while (slot < tail_final) {
                     if (slot < static_cast<unsigned>(L.F)) {
                         const unsigned long long w = ld_relaxed_u64(S.t_list + slot);
                         if (static_cast<uint32_t>(w >> 32) == tag) {
@@ -230,16 +315,29 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                             break;
                         }
                     }
-                    if (ld_relaxed_u32(qc + 2) == G_u && slot >= ld_relaxed_u32(qc + 0)) break;
+                    // every CTA's tail reservation returned before it counted itself as pushed
+                    if (ld_relaxed_u32(qc + 2) == G_u) tail_final = ld_relaxed_u32(qc + 0);
                 }
                 if (!got) break;
+                next = atomicAdd(qc + 1, 1u);
                 issue(static_cast<int32_t>(wv & ((1u << 27) - 1u)), wv >> 27);
+                if (n_stolen++ == 0) TLF(1, 2);
+                TLF(1, 3);
             }
-            // end-of-work sentinel for the consumers (completes the slot's phase, no bytes)
-            mbar_wait(&empty[st], ph ^ 1);
-            meta[st].idx = -1;
-            mbar_arrive(&full[st]);
-            TL(6, 4);
+#ifdef CD_TIMELINE
+            TLV(1, 7, (unsigned long long)n_own | ((unsigned long long)kept << 16) |
+                          ((unsigned long long)n_stolen << 32));
+#endif
+            // end-of-work sentinel for the consumers (completes the slot's phase, no bytes); split
+            // stage 3: one per dot warp (dot warp w takes every n_dot-th stage in sequence)
+            for (int k = 0; k < (kSplit3 ? n_dot : 1); ++k) {
+                mbar_wait(&empty[st], ph ^ 1);
+                meta[st].idx = -1;
+                meta[st].seq = pseq++;
+                mbar_arrive(&full[st]);
+                if (++st == nstages) { st = 0; ph ^= 1; }
+            }
+            TLF(6, 4);
         }
         __syncwarp();
     } else {
@@ -289,8 +387,16 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         }
         unsigned prev_actives = 0;  // thread 0: the previous launch's active count (in flight)
         if (threadIdx.x == 0) {
-            TL(5, 1);
+#ifdef CD_TIMELINE
+            tl_h1 = gtime();
+#endif
             const uint32_t t = static_cast<uint32_t>(__ldcg(S.ctl + kCtlEpoch)) + 1u;
+#ifdef CD_TIMELINE
+            tl_tag = t;
+            TLV(5, 0, tl_h0);
+            TLV(5, 1, tl_h1);
+            TLC(0);
+#endif
             cnt[NB + 1] = static_cast<int>(t);
             // own-work cap: the previous launch's active count spread over the grid (the first
             // launch keeps everything).  Only requested here -- it is consumed at the end of
@@ -327,6 +433,28 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                     for (int k = 0; k < 8; ++k) xr[b][j][k] *= inv;
             }
         }
+        if constexpr (kSplit3) {
+            // x (normalised) as f32 in shared memory for the stage-3 dot warps
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                const int vec = ct + j * nc;
+                if (vec < nvec) {
+                    float4* dst = reinterpret_cast<float4*>(xs + (int64_t)vec * kVec);
+                    dst[0] = make_float4(xr[0][j][0], xr[0][j][1], xr[0][j][2], xr[0][j][3]);
+                    dst[1] = make_float4(xr[0][j][4], xr[0][j][5], xr[0][j][6], xr[0][j][7]);
+                }
+            }
+        }
+#ifdef CD_TIMELINE
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int j = 0; j < VPT; ++j)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) asm volatile("" ::"f"(xr[0][j][k]));
+            TLF(0, 0);
+            TLC(1);
+        }
+#endif
         if (blockIdx.x == G - 1) {
             for (int64_t i = ct; i < (int64_t)nb * L.d; i += nc) y[i] = 0.0f;
             named_bar_sync(kBarC, nc);
@@ -337,12 +465,15 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         }
         named_bar_sync(kBarC, nc);
         const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
-        if (threadIdx.x == 0) TL(6, 2);
+#ifdef CD_TIMELINE
+        tl_tag = tag;
+#endif
+        if (threadIdx.x == 0) { TLF(6, 2); TLC(2); }
 
         // ---------------------------------------------------------- stage 1: latent columns
         if (nq > 0) {
             mbar_wait(bar_a, 0);
-            if (threadIdx.x == 0) TL(6, 3);
+            if (threadIdx.x == 0) { TLF(6, 3); TLC(3); }
             constexpr int kQ = 4;
             for (int qb = 0; qb < nq; qb += kQ) {
                 float v[kQ * NB];
@@ -369,20 +500,25 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                     for (int b = 0; b < NB; ++b) v[qq * NB + b] = a0[b] + a1[b];
                 }
                 constexpr int kV = kQ * NB;
+                if (threadIdx.x == 0 && qb == 0) { TLF(0, 1); TLC(4); }
                 const float tot = warp_transpose_sum<kV>(v);
                 if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
                 named_bar_sync(kBarC, nc);
+                if (threadIdx.x == 0 && qb == 0) { TLF(0, 2); TLC(5); }
                 if (warp == 0 && lane < kV) {
                     const int qq = lane / NB, b = lane % NB;
                     float s = 0.0f;
                     for (int w = 0; w < nwc; ++w) s += red[w * 32 + lane];
                     if (qb + qq < nq && b < nb)
-                        st_relaxed_u64(S.t_lat + b * L.ldr + q0 + qb + qq, tagged(tag, __float_as_uint(s)));
+                        for (int rp = 0; rp < P.lat_rep; ++rp)
+                            st_relaxed_u64(S.t_lat + (int64_t)rp * NB * L.ldr + b * L.ldr + q0 + qb + qq,
+                                           tagged(tag, __float_as_uint(s)));
                 }
                 named_bar_sync(kBarC, nc);
+                if (threadIdx.x == 0 && qb == 0) { TLF(0, 3); TLC(6); }
             }
         }
-        if (threadIdx.x == 0) TL(5, 2);
+        if (threadIdx.x == 0) TLF(5, 2);
         if (kRegB && P.b_smem) {
             // predictor rows smem -> registers while the latent columns of the other CTAs arrive
             if (nrows > 0) mbar_wait(bar_b, 0);
@@ -403,24 +539,25 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         // ---------------------------------------------------------- stage 2: predictor + compaction
         // gather the latent (every CTA published its columns as tagged words): all of a thread's
         // words are requested at once, stale ones re-polled
+        const unsigned long long* t_lat = S.t_lat + (int64_t)(blockIdx.x % P.lat_rep) * NB * L.ldr;
         for (int e0 = ct; e0 < NB * (int)L.ldr; e0 += 4 * nc) {
             unsigned long long w[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int e = e0 + k * nc;
                 const int b = e / (int)L.ldr, q = e % (int)L.ldr;
-                w[k] = (e < NB * (int)L.ldr && b < nb && q < L.r) ? ld_relaxed_u64(S.t_lat + e) : tagged(tag, 0u);
+                w[k] = (e < NB * (int)L.ldr && b < nb && q < L.r) ? ld_relaxed_u64(t_lat + e) : tagged(tag, 0u);
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int e = e0 + k * nc;
                 if (e >= NB * (int)L.ldr) continue;
-                if (static_cast<uint32_t>(w[k] >> 32) != tag) w[k] = tagged(tag, await_relaxed(S.t_lat + e, tag));
+                if (static_cast<uint32_t>(w[k] >> 32) != tag) w[k] = tagged(tag, await_relaxed(t_lat + e, tag));
                 latbuf[e] = __uint_as_float(static_cast<uint32_t>(w[k]));
             }
         }
         named_bar_sync(kBarC, nc);
-        if (threadIdx.x == 0) TL(5, 3);
+        if (threadIdx.x == 0) { TLF(5, 3); TLC(7); }
         if constexpr (kRegB) {
             float lat[NB][VPL][8];
 #pragma unroll
@@ -438,7 +575,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                     lat[b][v][4] = hi.x; lat[b][v][5] = hi.y; lat[b][v][6] = hi.z; lat[b][v][7] = hi.w;
                 }
             }
-            if (threadIdx.x == 0) TL(6, 0);
+            if (threadIdx.x == 0) TLF(6, 0);
             constexpr int kV = kRowsW * NB;
             float v[kV];
 #pragma unroll
@@ -511,7 +648,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             }
         }
         if (nrows > 0) mbar_wait(bar_b, 0);
-        if (threadIdx.x == 0) TL(6, 0);
+        if (threadIdx.x == 0) TLF(6, 0);
         {
             const W* base = reinterpret_cast<const W*>(ring);
             for (int rr0 = warp * kRBf; rr0 < nrows; rr0 += nwc * kRBf) {
@@ -571,19 +708,20 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         }
         }
         if (threadIdx.x == 0) {
-            TL(6, 1);
+            TLF(6, 1);
             cnt[NB + 2] = prev_actives > 0 ? static_cast<int>((prev_actives + G - 1) / G) : (1 << 30);
         }
         named_bar_sync(kBarC, nc);
-        if (threadIdx.x == 0) TL(5, 4);
+        if (threadIdx.x == 0) TLF(5, 4);
         named_bar_arrive(kBarK, nc + kWarp);  // producer may schedule stage 3 now
         if (threadIdx.x == 0) {
             st_relaxed_u64(S.t_alive + blockIdx.x * kMaxBatchFast, tagged(tag, static_cast<uint32_t>(cnt[1])));
             for (int b = 1; b < NB; ++b)
                 st_relaxed_u64(S.t_alive + blockIdx.x * kMaxBatchFast + b, tagged(tag, static_cast<uint32_t>(cnt[1 + b])));
             (void)await_acquire(S.t_count + kYZeroWord, tag);  // y zeroed (set long ago: one round trip)
-            TL(5, 5);
+            TLF(5, 5);
         }
+        if constexpr (!kSplit3) {
         int st = 0;
         uint32_t ph = 0;
 
@@ -617,11 +755,11 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
 #ifdef CD_TIMELINE
                     if (threadIdx.x == 0 && blockIdx.x < kTlCtas) {
                         const int rec = n_rec + q;
-                        if (rec == 0) TL(4, 0);
-                        if (rec == 3) TL(4, 1);
-                        if (rec == 6) TL(4, 2);
-                        TL(4, 3);
-                        g_timeline[4][blockIdx.x][7] = rec + 1;
+                        if (rec == 0) TLF(4, 0);
+                        if (rec == 3) TLF(4, 1);
+                        if (rec == 6) TLF(4, 2);
+                        TLF(4, 3);
+                        TLV(4, 7, rec + 1);
                     }
 #endif
                     const uint8_t* sb = ring + st * stage_bytes;
@@ -696,7 +834,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 }
             }
         }
-        if (threadIdx.x == 0) TL(5, 6);
+        if (threadIdx.x == 0) TLF(5, 6);
         if (n_rec > 0) {
             // this CTA's partial y -> shared memory (the ring is idle now) -> ONE bulk reduction
             // into global y by the TMA engine (cp.reduce.async.bulk .add.f32): line-granular
@@ -722,6 +860,121 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 bulk_commit_and_wait_read();
             }
         }
+        } else {
+        // ---------------------------------------------------------- stage 3 (split): batch 1, bf16
+        const int64_t row_bytes = L.ld * (int64_t)sizeof(W);
+        if (warp < n_dot) {
+            // dot warp: records warp, warp + n_dot, ... of the stage sequence
+            for (int e = warp;; e += n_dot) {
+                const int sq = e % nstages;
+                // the stage's previous use (e - nstages) may still be loading: its incomplete
+                // phase has the other parity, so the wait can return early -- retry until the
+                // stage holds record e
+                // (meta.seq == e implies the previous use completed, so the second wait is exact)
+                for (;;) {
+                    mbar_wait(&full[sq], static_cast<uint32_t>(e / nstages) & 1u);
+                    if (*reinterpret_cast<volatile int32_t*>(&meta[sq].seq) == e) break;
+                }
+                mbar_wait(&full[sq], static_cast<uint32_t>(e / nstages) & 1u);
+                if (meta[sq].idx < 0) {
+                    // this warp's sentinel: forward it (the down warps stop at the first one)
+                    if (lane == 0) mbar_arrive(&sready[sq]);
+                    break;
+                }
+#ifdef CD_TIMELINE
+                if (lane == 0 && blockIdx.x < kTlCtas) {
+                    if (e == 0) TLF(4, 0);
+                    if (e == 3) TLF(4, 1);
+                    if (e == 6) TLF(4, 2);
+                    TLF(4, 3);
+                    TLV(4, 7, e + 1);
+                }
+#endif
+                const W* rup = reinterpret_cast<const W*>(ring + sq * stage_bytes);
+                const W* rgate = reinterpret_cast<const W*>(ring + sq * stage_bytes + row_bytes);
+                float u0 = 0.f, u1 = 0.f, g0 = 0.f, g1 = 0.f;
+#pragma unroll 4
+                for (int v = lane; v < nvec; v += kWarp) {
+                    float wu[8], wg[8];
+                    Vec8<W>::load(rup + v * kVec, wu);
+                    Vec8<W>::load(rgate + v * kVec, wg);
+                    const float4 xa = reinterpret_cast<const float4*>(xs)[2 * v];
+                    const float4 xb = reinterpret_cast<const float4*>(xs)[2 * v + 1];
+                    const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+                    for (int k = 0; k < 8; k += 2) {
+                        ffma2(u0, u1, wu[k], wu[k + 1], xv[k], xv[k + 1]);
+                        ffma2(g0, g1, wg[k], wg[k + 1], xv[k], xv[k + 1]);
+                    }
+                }
+                float v2[2] = {u0 + u1, g0 + g1};
+                const float tot = warp_transpose_sum<2>(v2);  // lanes 0-15: u, 16-31: g
+                const float gsum = __shfl_sync(0xffffffffu, tot, 16);
+                __syncwarp();
+                if (lane == 0) {
+                    const bool alive = meta[sq].bits & 1u;
+                    svs[sq] = alive ? tot * act_fast(L.act, gsum) : 0.0f;
+                    mbar_arrive(&sready[sq]);  // release-orders the s store for the down warps
+                    mbar_arrive(&empty[sq]);
+                }
+            }
+        } else {
+            // down warps: column vectors td + j nd of y, every record in sequence
+            const int td = ct - n_dot * kWarp;
+            const int nd = (nwc - n_dot) * kWarp;
+            float yd[kVPD][8];
+#pragma unroll
+            for (int j = 0; j < kVPD; ++j)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) yd[j][k] = 0.0f;
+            int n_rec = 0;
+            for (int e = 0;; ++e) {
+                const int sq = e % nstages;
+                mbar_wait(&sready[sq], static_cast<uint32_t>(e / nstages) & 1u);
+                if (meta[sq].idx < 0) break;
+                const float sv = svs[sq];
+                const W* rdown = reinterpret_cast<const W*>(ring + sq * stage_bytes + 2 * row_bytes);
+#pragma unroll
+                for (int j = 0; j < kVPD; ++j) {
+                    const int vec = td + j * nd;
+                    if (vec < nvec) {
+                        float wd[8];
+                        Vec8<W>::load(rdown + vec * kVec, wd);
+#pragma unroll
+                        for (int k = 0; k < 8; k += 2) ffma2(yd[j][k], yd[j][k + 1], sv, sv, wd[k], wd[k + 1]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[sq]);
+                ++n_rec;
+            }
+            if (td == 0) TLF(5, 6);
+            if (n_rec > 0) {
+                // partial y -> shared memory (stage 0 of the ring: no record is in flight past the
+                // sentinel) -> one bulk reduction into global y
+                named_bar_sync(kBarD, nd);
+                float* ys = reinterpret_cast<float*>(ring);
+#pragma unroll
+                for (int j = 0; j < kVPD; ++j) {
+                    const int vec = td + j * nd;
+                    if (vec < nvec)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int64_t col = (int64_t)vec * kVec + k;
+                            if (col < L.d) ys[col] = yd[j][k];
+                        }
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(kBarD, nd);
+                if (td == 0) {
+                    (void)await_acquire(S.t_count + kYZeroWord, tag);  // y zeroed
+                    bulk_reduce_add_f32(y, ys, static_cast<uint32_t>(L.d * sizeof(float)));
+                    bulk_commit_and_wait_read();
+                }
+            }
+            if (td == 0) TLF(5, 7);
+        }
+        }
         if (blockIdx.x == 0 && warp == 0) {
             // per-sample alive counts (sum of the CTAs' tagged counts), then advance the tag:
             // every CTA read it before publishing the count CTA 0's producer waited for
@@ -737,21 +990,33 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             if (lane == 0) S.ctl[kCtlEpoch] = tag;
         }
     }
-    if (threadIdx.x == 0) {
-        TL(5, 7);
-    }
+    if (!kSplit3 && threadIdx.x == 0) TLF(5, 7);
 }
 
 }  // namespace
 
 #ifdef CD_TIMELINE
+// The second most recent launch (its successor's prologue overlapped its tail: steady state).
 cudaError_t read_timeline_fused(unsigned long long* out, int64_t n) {
     const size_t cnt = (size_t)kTlKernels * kTlCtas * kTlPhases;
     if ((size_t)n < cnt) return cudaErrorInvalidValue;
-    cudaError_t e = cudaMemcpyFromSymbol(out, g_timeline, cnt * sizeof(unsigned long long));
-    static unsigned long long zeros[kTlKernels * kTlCtas * kTlPhases];
-    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_timeline, zeros, sizeof(zeros));
-    return e;
+    static unsigned long long all[4 * kTlKernels * kTlCtas * kTlPhases];
+    cudaError_t e = cudaMemcpyFromSymbol(all, g_tlf, sizeof(all));
+    if (e != cudaSuccess) return e;
+    unsigned long long last[4] = {0, 0, 0, 0};
+    for (int sl = 0; sl < 4; ++sl)
+        for (int c = 0; c < kTlCtas; ++c) {
+            const unsigned long long v = all[((size_t)(sl * kTlKernels + 5) * kTlCtas + c) * kTlPhases + 1];
+            if (v > last[sl]) last[sl] = v;
+        }
+    int best = 0, second = -1;
+    for (int sl = 1; sl < 4; ++sl) if (last[sl] > last[best]) best = sl;
+    for (int sl = 0; sl < 4; ++sl)
+        if (sl != best && last[sl] > 0 && (second < 0 || last[sl] > last[second])) second = sl;
+    const int pick = second >= 0 ? second : best;
+    for (size_t i = 0; i < cnt; ++i) out[i] = all[pick * cnt + i];
+    static unsigned long long zeros[4 * kTlKernels * kTlCtas * kTlPhases];
+    return cudaMemcpyToSymbol(g_tlf, zeros, sizeof(zeros));
 }
 #else
 cudaError_t read_timeline_fused(unsigned long long*, int64_t) { return cudaErrorNotSupported; }
@@ -787,14 +1052,21 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     // predictor rows at 8 per warp; at most 15 (+ the producer warp = 512 threads)
     int64_t nwc64 = std::max<int64_t>(8, ((nvec + vpt - 1) / vpt + kWarp - 1) / kWarp);
     if (regb) nwc64 = std::max<int64_t>(nwc64, (rpc + 7) / 8);
+    // split stage 3 (batch 1, bf16): 8 down warps own the columns (<= 4 vectors each), the
+    // other consumer warps (>= 2) compute the records' dots
+    const bool split3 = regb && nbk == 1;
+    if (split3) nwc64 = std::max<int64_t>(nwc64, 10);
     const int nwc = static_cast<int>(nwc64);
+    const int n_dot = split3 ? nwc - 8 : 0;
+    if (split3 && (nvec + 8 * kWarp - 1) / (8 * kWarp) > 4) return cudaErrorInvalidValue;
     if (nwc * kWarp > kMaxConsumers) return cudaErrorInvalidValue;
     const int threads = (nwc + 1) * kWarp;
     // fixed carve-up beside the ring: latent, barriers, meta, lists, scratch, latent fragments
     // (the theta_at slice is overlaid on the ring's tail)
     const int64_t aux_bytes = (int64_t)qrows * L.ld * esz;
     const int64_t fixed = (int64_t)nbk * L.ldr * 4 + 3 * 8 + (int64_t)rpc * 8 + (nwc * 32 + kGroupF * nbk) * 4 +
-                          (4 + nbk) * 4 + nwc * nbk * 4 + 64;
+                          (4 + nbk) * 4 + nwc * nbk * 4 + 64 +
+                          (split3 ? 12 * 12 + L.ld * 4 + 32 : 0);  // s hand-over (<= 12 stages), x f32
     const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
     const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
     if (nstages < 2) return cudaErrorInvalidValue;
@@ -825,6 +1097,9 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
         p.rows_per_cta = rpc;
         p.qrows = qrows;
         p.b_smem = b_smem;
+        p.n_dot = n_dot;
+        p.lat_rep = 1;
+        while (p.lat_rep < CD_LAT_REP && (int64_t)p.lat_rep * 2 * nbk * L.ldr <= kMaxBatchFast * 2048) p.lat_rep *= 2;
         return launch_ex(kern, dim3(G), dim3(threads), smem, c, true, p);
     };
 #define CD_FUSED_CASES(W)                                          \

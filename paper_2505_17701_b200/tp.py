@@ -98,14 +98,15 @@ class TPStack:
     whole step is capturable in one CUDA graph."""
 
     def __init__(self, tps: "list[TPLayer]", taus, eps: float = RMS_EPS, group=None,
-                 method: int = _capi.METHOD_DC):
+                 method: int = _capi.METHOD_DC, prefetch: bool = False):
         if not tps or len(tps) != len(taus):
             raise DataError("TPStack: need one threshold per layer")
         self.tps = list(tps)
         self.taus = [float(t) for t in taus]
-        if method == _capi.METHOD_DC:
+        if method == _capi.METHOD_DC and prefetch:
             # a step runs the layers in order (then layer 0 of the next step): each layer
-            # L2-prefetches the next one's predictor under its own record stream
+            # L2-prefetches the next one's predictor (measured slower on the B200 at the Llama
+            # shape: the prefetch traffic delays the next step's latency-bound chain)
             for l, t in enumerate(self.tps):
                 t.dev.set_prefetch(self.tps[(l + 1) % len(self.tps)].dev)
         self.eps, self.group, self.method = float(eps), group, method

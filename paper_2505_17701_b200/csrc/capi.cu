@@ -109,8 +109,7 @@ struct cd_layer {
     bool weights_finite = true;  // every uploaded weight finite: the row-union GEMM may read any row
     const void* pf_at = nullptr;  // cd_layer_set_prefetch: the next layer's predictor (L2 prefetch)
     const void* pf_bt = nullptr;
-    cublasHandle_t blas = nullptr;
-    Grow tc_ws, blas_ws;    // tensor-core path workspace; cuBLAS workspace (graph-capture safe)
+    Grow tc_ws;             // tensor-core path workspace
     Grow rms_ws;            // RMS-normalised inputs for the engines that do not fuse the norm
     // host-call CUDA graph: [H2D inputs, kernels, D2H outputs] replayed while the call signature
     // (method, batch, tau, options) repeats -- one launch instead of four API calls per step
@@ -176,7 +175,6 @@ struct cd_layer {
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
         }
-        if (blas) cublasDestroy(blas);
         if (hg.exec) cudaGraphExecDestroy(hg.exec);
         for (auto& a : dev_allocs) cudaFree(a.first);
         for (void* p : host_allocs) cudaFreeHost(p);
@@ -274,15 +272,6 @@ bool tc_eligible(const cd_layer* h, const Req& r) {
     return r.method != cdk::kDC || h->L.theta_bt;
 }
 
-cublasHandle_t blas_of(cd_layer* h) {
-    if (!h->blas) {
-        if (cublasCreate(&h->blas) != CUBLAS_STATUS_SUCCESS) fail(CD_ERR_CUDA, "cublasCreate failed");
-        const size_t ws = 32u << 20;
-        if (cublasSetWorkspace(h->blas, h->blas_ws.get<uint8_t>(ws), ws) != CUBLAS_STATUS_SUCCESS)
-            fail(CD_ERR_CUDA, "cublasSetWorkspace failed");
-    }
-    return h->blas;
-}
 
 // Enqueue one operator call (device pointers) on r.stream.  Returns the number of launches.
 int run_chain(cd_layer* h, const Req& r) {
@@ -319,12 +308,15 @@ int run_chain(cd_layer* h, const Req& r) {
         const cdk::tc::Plan p = cdk::tc::plan_for(r.nb, r.method);
         void* ws = h->tc_ws.get<uint8_t>(cdk::tc::workspace_bytes(L, p, c.num_sms));
         const uint8_t* ovr = r.with_masks ? r.masks_in : r.ovr;
-        ck(cdk::tc::launch_batched(L, p, ws, S.tc_flags, blas_of(h), r.method, r.nb, r.x, r.tau, ovr, r.y, r.mask_out,
+        ck(cdk::tc::launch_batched(L, p, ws, S.tc_flags, r.method, r.nb, r.x, r.tau, ovr, r.y, r.mask_out,
                                    r.ind_out, r.alive_out, c),
            "batched (tensor cores)");
         h->last_path = CD_PATH_TENSOR;
-        // own kernels: x pack, [latent fold], gate/up, down (+ the cuBLAS latent GEMM for DC)
-        return 3 + (r.method == cdk::kDC && !ovr ? 1 : 0);
+        if (p.split) return 1;  // decode: one persistent kernel (k_tc_fused)
+        // prefill: x pack, gate/up, [zero of the stream-K tiles], down
+        const int64_t tiles = ((r.nb + 255) / 256) * ((d + 255) / 256);
+        const int64_t grid = std::min<int64_t>(c.num_sms, cdk::kMaxCtas);
+        return 3 + (tiles % grid != 0 ? 1 : 0);
     }
     h->last_path = r.reduction == CD_REDUCTION_UNORDERED ? CD_PATH_FAST : CD_PATH_EXACT;
     if (r.reduction == CD_REDUCTION_UNORDERED) {
@@ -757,7 +749,7 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
     std::lock_guard<std::recursive_mutex> dlock(ctx.mu);
     h->stream = ctx.stream;
     h->dev_mu = &ctx.mu;
-    for (Grow* g : {&h->tc_ws, &h->blas_ws, &h->rms_ws, &h->g_dx, &h->g_dy, &h->g_dmask_in, &h->g_dmask_out, &h->g_du_in,
+    for (Grow* g : {&h->tc_ws, &h->rms_ws, &h->g_dx, &h->g_dy, &h->g_dmask_in, &h->g_dmask_out, &h->g_du_in,
                     &h->g_dind, &h->g_dalive, &h->g_hx, &h->g_hy, &h->g_hmask, &h->g_hind, &h->g_halive})
         g->gen = &h->gen;
     cdk::LayerDev& L = h->L;

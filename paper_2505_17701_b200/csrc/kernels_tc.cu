@@ -19,7 +19,6 @@
 // f32 accumulation dominates: the result matches the CUDA-core path to ~1e-5 relative, and the
 // thresholds see the same logits.  Prefill (large token counts, dense) uses plain bf16
 // activations (standard bf16 inference numerics, 1e-2 bound).
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -369,52 +368,80 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
     }
 }
 
-// ---------------------------------------------------------------- phase B kernel
+// ---------------------------------------------------------------- prefill down projection
 //
-// y (nb x d, f32, zeroed) += s W_down.  UMMA view: D[j][b] = sum_i W_down[i][j] s[b][i], so
-// A = W_down^T is MN-major (d is the contiguous dimension of each neuron's down row; TMA boxes of
-// 64 j x 64 i, 128B-swizzled), B = the s rows (K-major).  In split mode the hi and lo rows of s
-// are two MMAs into the SAME accumulator (D = W^T (s_hi + s_lo)^T), so no fold pass.  Tiles are
-// (128-column j-tile, n-tile), k-blocks 64 neurons; the same stream-K ranges as phase A, each
-// segment's partial reduced into y with red.global.add (TMEM double-buffered: segments do not
-// wait for each other's drain).
-constexpr int kDJ = 2;  // 128-column j sub-tiles per CTA tile (they share the s tile)
+// Y (nb x d, f32) = S W_down for dense prefill (weighted_sum / forward_dense, gated_mlp.cpp:28-59,
+// over a token block): a plain compute-bound GEMM, M = tokens, N = d, K = F.
+//   A = S rows (K-major, bf16, written by the gate/up kernel), TMA boxes 64 K x 128 tokens.
+//   B = W_down as [F][d]: d contiguous in each neuron's down row, so B is MN-major; TMA boxes
+//       64 d x 64 K, 128B-swizzled, four per 256-column tile (descriptor LBO = one box, 8 KB).
+// CTA tile 256 tokens x 256 columns: two UMMA M=128 N=256 accumulators (the whole 512-column
+// TMEM), each k-block loads 2 x 16 KB of A and 32 KB of B -- 64 KB per 2 x 4.2 MFLOP, the
+// L2->SM feed that bounds a single-CTA tile.  Three 64 KB ring stages.
+// Schedule: whole tiles first (tile t on CTA t mod G while a full wave remains: plain v4 stores),
+// then the remaining tiles' k-blocks split evenly over all CTAs (stream-K, red.global.add.v4 into
+// rows zeroed by k_tc_zero_tiles).  Epilogue: 8 warps, warp w drains TMEM lane quarter w % 4 of
+// accumulator (w - 2) / 4, 16 columns per tcgen05.ld.
+constexpr int kPfN = 256;                       // columns (d) per tile
+constexpr int kPfM = 256;                       // tokens per tile (two M=128 accumulators)
+constexpr int kPfStage = 2 * kABytes + 4 * kBK * kBK * 2;  // 64 KB
+
+struct PfDownArgs {
+    int nb = 0, d = 0;
+    int nkb = 0;            // 64-neuron k-blocks
+    int n_tt = 0, n_jt = 0; // token tiles, column tiles
+    int n_full = 0;         // tiles done whole (a multiple of the grid), the rest stream-K
+    int stages = 0;
+    float* y = nullptr;
+};
+
+struct PfSeg {
+    int tile, kb0, kb1;
+    bool whole;
+};
+
+// Segment si of CTA c: its whole tiles c, c + G, ... < n_full, then its stream-K range over the
+// remaining tiles' k-blocks.
+__device__ __forceinline__ bool pf_seg(int c, int si, int G, const PfDownArgs& a, PfSeg& sg) {
+    const int n_whole = a.n_full > c ? (a.n_full - c + G - 1) / G : 0;
+    if (si < n_whole) {
+        sg = {c + si * G, 0, a.nkb, true};
+        return true;
+    }
+    const int tiles = a.n_tt * a.n_jt;
+    const int64_t U = static_cast<int64_t>(tiles - a.n_full) * a.nkb;
+    Seg s2;
+    if (U <= 0 || !seg_at(c, si - n_whole, U, G, a.nkb, s2)) return false;
+    sg = {a.n_full + s2.tile, s2.kb0, s2.kb1, false};
+    return true;
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
-k_tc_down(const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUtensorMap m_s, const DownArgs a) {
+k_tc_pf_down(const __grid_constant__ CUtensorMap m_s, const __grid_constant__ CUtensorMap m_w, const PfDownArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int nbt = a.nbt;
-    const int brows = 2 * nbt;                    // B rows per stage: hi rows, then lo rows
-    constexpr int kABytesD = kDJ * kBM * kBK * 2;  // 2 x (two 64 x 64 boxes of W_down)
-    const int stage_bytes = kABytesD + brows * kBK * 2;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * kPfStage);
     uint64_t* empty = full + a.stages;
-    uint64_t* tfull = empty + a.stages;  // [2]
-    uint64_t* tempty = tfull + 2;        // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
+    uint64_t* tfull = empty + a.stages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nkb = a.kb;
     const int G = gridDim.x, c = blockIdx.x;
-    const int64_t U = static_cast<int64_t>(a.tiles) * nkb;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(tfull + b, 1);
-            mbar_init(tempty + b, kEpiThreads);
-        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, kEpiThreads);
         fence_mbar_init();
-        prefetch_map(&m_w);
         prefetch_map(&m_s);
+        prefetch_map(&m_w);
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(a.tmem_cols)
+                     "r"(512)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -422,97 +449,120 @@ k_tc_down(const __grid_constant__ CUtensorMap m_w, const __grid_constant__ CUten
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // S comes from the gate/up kernel
 
     if (warp == 0) {
         if (lane == 0) {
-            const uint64_t pw = policy_evict_first();
-            const uint64_t ps = policy_evict_last();
+            const uint64_t ps = policy_evict_first();  // S: read once per column tile
+            const uint64_t pw = policy_evict_last();   // W_down: re-read by every token tile
             int it = 0;
-            Seg sg;
-            for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
-                const int j0 = (sg.tile / a.n_tiles) * kDJ * kBM;
-                const int row0 = (sg.tile % a.n_tiles) * brows;
+            PfSeg sg;
+            for (int si = 0; pf_seg(c, si, G, a, sg); ++si) {
+                const int tt = sg.tile / a.n_jt, jt = sg.tile % a.n_jt;
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
                     const int s = it % a.stages;
                     if (it >= a.stages) mbar_wait(empty + s, ((it / a.stages) - 1) & 1);
-                    uint8_t* st = smem + s * stage_bytes;
-                    mbar_arrive_expect_tx(full + s, kABytesD + brows * kBK * 2);
+                    uint8_t* st = smem + s * kPfStage;
+                    mbar_arrive_expect_tx(full + s, kPfStage);
+                    tma_load_2d(st, &m_s, kb * kBK, tt * kPfM, full + s, ps);
+                    tma_load_2d(st + kABytes, &m_s, kb * kBK, tt * kPfM + kBM, full + s, ps);
 #pragma unroll
-                    for (int q = 0; q < 2 * kDJ; ++q)
-                        tma_load_2d(st + q * (kBK * kBK * 2), &m_w, j0 + 64 * q, kb * kBK, full + s, pw);
-                    tma_load_2d(st + kABytesD, &m_s, kb * kBK, row0, full + s, ps);
+                    for (int q = 0; q < 4; ++q)
+                        tma_load_2d(st + 2 * kABytes + q * (kBK * kBK * 2), &m_w, jt * kPfN + 64 * q, kb * kBK,
+                                    full + s, pw);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            // D_q[j][b]: M = 128 j (A MN-major), N = nbt samples; q = j sub-tile
-            const uint32_t idesc = idesc_bf16(kBM, nbt) | (1u << 15);
+            // D[m][n] = sum_k S[m][k] W[k][n]: A K-major, B MN-major (bit 16), M = 128, N = 256
+            const uint32_t idesc = idesc_bf16(kBM, kPfN) | (1u << 16);
             int it = 0;
-            Seg sg;
-            for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
-                const int buf = si & 1;
-                if (si >= 2) {
-                    mbar_wait(tempty + buf, ((si >> 1) - 1) & 1);
+            PfSeg sg;
+            for (int si = 0; pf_seg(c, si, G, a, sg); ++si) {
+                if (si >= 1) {
+                    mbar_wait(tempty, (si - 1) & 1);  // the previous segment's accumulators drained
                     tc_fence_after();
                 }
-                const uint32_t td = tmem + buf * kDJ * nbt;
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
                     const int s = it % a.stages;
                     mbar_wait(full + s, (it / a.stages) & 1);
                     tc_fence_after();
-                    const uint32_t base = smem_u32(smem + s * stage_bytes);
-                    const uint64_t dbh = sw128_desc(base + kABytesD);
-                    const uint64_t dbl = sw128_desc(base + kABytesD + nbt * kBK * 2);
+                    const uint32_t base = smem_u32(smem + s * kPfStage);
+                    const uint64_t db = sw128_mn_desc(base + 2 * kABytes, kBK * kBK * 2);
 #pragma unroll
-                    for (int q = 0; q < kDJ; ++q) {
-                        const uint64_t da = sw128_mn_desc(base + q * kBM * kBK * 2, kBK * kBK * 2);
+                    for (int k = 0; k < kBK / 16; ++k) {
 #pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k) {
-                            // A: 16 K-rows of 128 B per step (+2048 B); B: +32 B inside the swizzle atom
-                            const uint64_t oa = static_cast<uint64_t>(128 * k), ob = static_cast<uint64_t>(2 * k);
-                            umma_bf16(td + q * nbt, da + oa, dbh + ob, idesc, (kb > sg.kb0 || k > 0) ? 1u : 0u);
-                            umma_bf16(td + q * nbt, da + oa, dbl + ob, idesc, 1u);
+                        for (int h = 0; h < 2; ++h) {
+                            const uint64_t da = sw128_desc(base + h * kABytes);
+                            // A: +32 B inside the swizzle atom per K=16; B: 16 K-rows of 128 B (+2 KB)
+                            umma_bf16(tmem + h * kPfN, da + static_cast<uint64_t>(2 * k), db + static_cast<uint64_t>(128 * k),
+                                      idesc, (kb > sg.kb0 || k > 0) ? 1u : 0u);
                         }
                     }
                     umma_commit(empty + s);
                 }
-                umma_commit(tfull + buf);
+                umma_commit(tfull);
             }
         }
     } else {
-        // epilogue: row j of a sub-tile = TMEM lane; warp half q takes sub-tile q
+        // epilogue: warp w -> TMEM lanes 32 (w % 4) .. +31 (tokens) of accumulator h
         const int g = warp & 3;
-        const int q = (warp - 2) >> 2;
-        const int m = g * 32 + lane;
-        const uint32_t trow = tmem + (static_cast<uint32_t>(g * 32) << 16);
-        Seg sg;
-        for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
-            const int buf = si & 1;
-            mbar_wait(tfull + buf, (si >> 1) & 1);
+        const int h = (warp - 2) >> 2;
+        const uint32_t trow = tmem + (static_cast<uint32_t>(g * 32) << 16) + h * kPfN;
+        PfSeg sg;
+        for (int si = 0; pf_seg(c, si, G, a, sg); ++si) {
+            mbar_wait(tfull, si & 1);
             tc_fence_after();
-            const int j = (sg.tile / a.n_tiles) * kDJ * kBM + q * kBM + m;
-            const int64_t gb0 = static_cast<int64_t>(sg.tile % a.n_tiles) * nbt;
-            for (int cb = 0; cb < nbt; cb += 8) {
-                float v[8];
-                tmem_ld8(trow + (buf * kDJ + q) * nbt + cb, v);
+            const int tt = sg.tile / a.n_jt, jt = sg.tile % a.n_jt;
+            const int64_t tok = static_cast<int64_t>(tt) * kPfM + h * kBM + g * 32 + lane;
+            float* yrow = a.y + tok * a.d + jt * kPfN;
+            const bool row_ok = tok < a.nb;
+            const int ncols = min(kPfN, a.d - jt * kPfN);
+            for (int cb = 0; cb < kPfN; cb += 16) {
+                float v[16];
+                tmem_ld16(trow + cb, v);
                 tmem_wait_ld();
-                if (j < a.d) {
+                if (row_ok && cb < ncols && (a.d & 3) != 0) {
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        const int64_t b = gb0 + cb + t;
-                        if (b < a.nb) red_add_f32(a.y + b * a.d + j, v[t]);
+                    for (int q = 0; q < 16; ++q) {
+                        if (cb + q >= ncols) continue;
+                        if (sg.whole) yrow[cb + q] = v[q];
+                        else red_add_f32(yrow + cb + q, v[q]);
+                    }
+                } else if (row_ok && cb < ncols) {
+                    if (sg.whole) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (cb + 4 * q < ncols)
+                                *reinterpret_cast<float4*>(yrow + cb + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (cb + 4 * q < ncols) red_add_v4(yrow + cb + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                     }
                 }
             }
             tc_fence_before();
-            mbar_arrive(tempty + buf);
+            mbar_arrive(tempty);
         }
     }
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    }
+}
+
+// Zero the stream-K tiles' blocks of y (tile-major from `first`): grid (tiles, 256 / 8) x 256 threads.
+__global__ void k_tc_zero_tiles(float* __restrict__ y, int nb, int d, int n_jt, int first) {
+    const int t = first + blockIdx.x;
+    const int tt = t / n_jt, jt = t % n_jt;
+    const int c0 = jt * kPfN, ncols = min(kPfN, d - c0);
+    for (int r = blockIdx.y * 8 + threadIdx.x / 32; r < kPfM; r += gridDim.y * 8) {
+        const int64_t tok = static_cast<int64_t>(tt) * kPfM + r;
+        if (tok >= nb) break;
+        for (int cc = threadIdx.x % 32; cc < ncols; cc += 32) y[tok * d + c0 + cc] = 0.0f;
     }
 }
 
@@ -553,34 +603,6 @@ __global__ void k_tc_pack_x(const float* __restrict__ x, int64_t d, int64_t ld, 
     }
 }
 
-// Latent pairs from the f32 GEMM output: fold hi + lo rows, re-split into bf16 pairs.
-__global__ void k_tc_fold_split(const float* __restrict__ in, int64_t ldi, int64_t ncols, int nbt,
-                                __nv_bfloat16* __restrict__ outp, int64_t ldo) {
-    const int64_t b = blockIdx.y;
-    const int64_t r = (b / nbt) * 2 * nbt + b % nbt;
-    for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < ncols;
-         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const float v = in[r * ldi + c] + in[(r + nbt) * ldi + c];
-        const __nv_bfloat16 h = __float2bfloat16_rn(v);
-        outp[r * ldo + c] = h;
-        outp[(r + nbt) * ldo + c] = __float2bfloat16_rn(v - __bfloat162float(h));
-    }
-}
-
-
-// ---------------------------------------------------------------- host: tensor maps, cuBLAS
-cudaError_t cublas_status(cublasStatus_t s) { return s == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown; }
-
-// Row-major C (rows x n, ldc) = A (rows x k, lda) * W, W k x n row-major (ldw).
-cudaError_t gemm_rows_w(cublasHandle_t h, int64_t rows, int64_t n, int64_t k, const void* A, int64_t lda,
-                        const void* W, int64_t ldw, float* C, int64_t ldc) {
-    const float one = 1.0f, zero = 0.0f;
-    return cublas_status(cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows),
-                                      static_cast<int>(k), &one, W, CUDA_R_16BF, static_cast<int>(ldw), A,
-                                      CUDA_R_16BF, static_cast<int>(lda), &zero, C, CUDA_R_32F,
-                                      static_cast<int>(ldc), CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
-}
-
 }  // namespace
 
 int64_t round_up64(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
@@ -613,17 +635,17 @@ size_t workspace_bytes(const LayerDev& L, const Plan& p, int num_sms) {
     return b;
 }
 
-cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned* flags, cublasHandle_t blas,
-                           int method, int64_t nb,
+cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned* flags, int method, int64_t nb,
                            const float* x, float tau, const uint8_t* ovr, float* y, uint8_t* mask_out,
                            float* ind_out, int* alive_out, const LaunchCfg& c) {
     if (L.dtype != 1 /* bf16 */ || !L.w_up) return cudaErrorInvalidValue;
     if (method == kDC && !ovr && !L.theta_bt) return cudaErrorInvalidValue;
-    static const bool fused_env = dev_knob("CD_TC_FUSED", 1) != 0;
-    if (p.split && fused_env)
+    // decode (activations as bf16 pairs): one persistent kernel, kernels_tc_fused.cu
+    if (p.split)
         return launch_batched_fused(L, p, ws, workspace_bytes(L, p, c.num_sms), flags, method, nb, x, tau, ovr, y,
                                     mask_out, ind_out, alive_out, c);
-    const int64_t ldr = L.ldr > 0 ? L.ldr : 8;
+    // dense prefill: gate/up (k_tc_gateup, s as plain bf16 rows) then y = s W_down (k_tc_pf_down)
+    if (method != kDense || ovr) return cudaErrorInvalidValue;
     const int64_t ld_s = round_up64(L.F, 8);
     uint8_t* w = static_cast<uint8_t*>(ws);
     auto take = [&](size_t bytes) {
@@ -633,123 +655,77 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     };
     auto* xb = reinterpret_cast<__nv_bfloat16*>(take(p.rows * L.ld * 2));
     auto* sb = reinterpret_cast<__nv_bfloat16*>(take(p.rows * ld_s * 2));
-    auto* latb = reinterpret_cast<__nv_bfloat16*>(take(p.rows * ldr * 2));
-    auto* lat32 = reinterpret_cast<float*>(take(p.rows * ldr * 4));
+    const int64_t ldr = L.ldr > 0 ? L.ldr : 8;
+    (void)take(p.rows * ldr * 2);
+    (void)take(p.rows * ldr * 4);
     auto* ws_partial = reinterpret_cast<float*>(take(static_cast<size_t>(c.num_sms) * 3 * p.N * kBM * 4));
-    const bool dc_pred = method == kDC && !ovr;
 
     cudaError_t e = cudaSuccess;
-    if (cublasSetStream(blas, c.stream) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
     k_tc_pack_x<<<dim3(static_cast<unsigned>((L.d + 1023) / 1024), static_cast<unsigned>(nb)), 256, 0, c.stream>>>(
-        x, L.d, L.ld, p.split, p.nbt, xb);
+        x, L.d, L.ld, 0, p.nbt, xb);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (dc_pred) {
-        // latent pairs = x theta_a (theta_a is d x ldr row-major, the reference layout)
-        e = gemm_rows_w(blas, p.rows, L.r, L.d, xb, L.ld, L.theta_a, ldr, lat32, ldr);
-        if (e != cudaSuccess) return e;
-        k_tc_fold_split<<<dim3(static_cast<unsigned>((L.r + 255) / 256), static_cast<unsigned>(nb)), 256, 0,
-                          c.stream>>>(lat32, ldr, L.r, p.nbt, latb, ldr);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
     if (alive_out && (e = cudaMemsetAsync(alive_out, 0, sizeof(int) * nb, c.stream)) != cudaSuccess) return e;
 
-    CUtensorMap m_up, m_gate, m_x, m_tb, m_lat;
-    bool ok = make_map(&m_up, L.w_up, L.F, L.d, L.rs, kBM) && make_map(&m_gate, L.w_gate, L.F, L.d, L.rs, kBM) &&
-              make_map(&m_x, xb, p.rows, L.d, L.ld, p.N);
-    if (dc_pred) {
-        ok = ok && make_map(&m_tb, L.theta_bt, L.F, L.r, ldr, kBM) && make_map(&m_lat, latb, p.rows, L.r, ldr, p.N);
-    } else {
-        m_tb = m_up;
-        m_lat = m_x;
-    }
-    if (!ok) return cudaErrorInvalidValue;
-
+    CUtensorMap m_up, m_gate, m_x;
+    if (!make_map(&m_up, L.w_up, L.F, L.d, L.rs, kBM) || !make_map(&m_gate, L.w_gate, L.F, L.d, L.rs, kBM) ||
+        !make_map(&m_x, xb, p.rows, L.d, L.ld, p.N))
+        return cudaErrorInvalidValue;
     GateUpArgs a;
     a.F = static_cast<int>(L.F);
     a.nb = static_cast<int>(nb);
     a.nbt = p.nbt;
     a.N = p.N;
     a.kb_x = static_cast<int>((L.d + kBK - 1) / kBK);
-    a.kb_z = dc_pred ? static_cast<int>((L.r + kBK - 1) / kBK) : 0;
+    a.kb_z = 0;
     a.tau = tau;
-    static const int st_env = dev_knob("CD_TC_STAGES", 0);
-    a.ovr = ovr;
+    a.ovr = nullptr;
     a.s_out = sb;
     a.ld_s = ld_s;
     a.mask_out = mask_out;
     a.ind_out = ind_out;
     a.alive_out = alive_out;
-    const int used_cols = (dc_pred ? 3 : 2) * p.N;
-    a.tmem_cols = used_cols <= 32 ? 32 : used_cols <= 64 ? 64 : used_cols <= 128 ? 128 : used_cols <= 256 ? 256 : 512;
-    if (used_cols > 512) return cudaErrorInvalidValue;
+    a.tmem_cols = 2 * p.N <= 256 ? 256 : 512;
+    if (2 * p.N > 512) return cudaErrorInvalidValue;
     a.n_tiles = p.n_tiles;
     a.tiles = static_cast<int>((L.F + kBM - 1) / kBM) * p.n_tiles;
-    const int64_t units = static_cast<int64_t>(a.tiles) * (a.kb_x + a.kb_z);
-    static const int grid_env = dev_knob("CD_TC_GRID", 0);
-    static unsigned long long* tl_env = []() -> unsigned long long* {
-#ifdef CD_TIMELINE  // development builds only: a device address taken from the environment
-        const char* e = std::getenv("CD_TC_TL");
-        return e ? reinterpret_cast<unsigned long long*>(std::strtoull(e, nullptr, 10)) : nullptr;
-#else
-        return nullptr;
-#endif
-    }();
-    a.tl = tl_env;
-    int grid = static_cast<int>(std::min<int64_t>(std::min(c.num_sms, kMaxCtas), units));
-    if (grid_env > 0 && grid_env < grid) grid = grid_env;
+    const int64_t units = static_cast<int64_t>(a.tiles) * a.kb_x;
+    a.tl = nullptr;
+    const int grid = static_cast<int>(std::min<int64_t>(std::min(c.num_sms, kMaxCtas), units));
     a.ws = ws_partial;
     a.flags = flags;
     const int stage_bytes = 2 * kABytes + p.N * kBK * 2;
     const size_t fixed = 1024 + 256;
     a.stages = static_cast<int>(std::min<size_t>(8, (kMaxDynSmem - fixed) / stage_bytes));
-    if (st_env > 0) a.stages = std::min(a.stages, st_env);
     const size_t smem = fixed + static_cast<size_t>(a.stages) * stage_bytes;
-    using KFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GateUpArgs);
-    const int kind = ovr ? kOvr : method;
-    KFn fn = nullptr;
-#define CD_TC_PICK(K, S)                                                                      \
-    if (kind == K && p.split == S) fn = L.act == 0 ? k_tc_gateup<K, S, 0> : k_tc_gateup<K, S, 1>;
-    CD_TC_PICK(kDense, true)
-    CD_TC_PICK(kDense, false)
-    CD_TC_PICK(kMC, true)
-    CD_TC_PICK(kDC, true)
-    CD_TC_PICK(kCATS, true)
-    CD_TC_PICK(kOvr, true)
-#undef CD_TC_PICK
-    if (!fn) return cudaErrorInvalidValue;
+    auto fn = L.act == 0 ? k_tc_gateup<kDense, false, 0> : k_tc_gateup<kDense, false, 1>;
     if ((e = set_smem(fn, smem)) != cudaSuccess) return e;
+    CUtensorMap m_tb = m_up, m_lat = m_x;
     fn<<<grid, kThreads, smem, c.stream>>>(m_up, m_gate, m_x, m_tb, m_lat, a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
-    // phase B: y = s W_down (W_down rows are the third part of each neuron record, stride rs).
-    // Prefill (no split) is a compute-bound plain GEMM: cuBLAS.
-    if (!p.split) return gemm_rows_w(blas, nb, L.d, L.F, sb, ld_s, L.w_down, L.rs, y, L.d);
-    if ((e = cudaMemsetAsync(y, 0, sizeof(float) * nb * L.d, c.stream)) != cudaSuccess) return e;
-    DownArgs b;
-    b.d = static_cast<int>(L.d);
+    // y = s W_down (W_down rows are the third part of each neuron record, stride rs)
+    PfDownArgs b;
     b.nb = static_cast<int>(nb);
-    b.nbt = p.nbt;
-    b.n_tiles = p.n_tiles;
-    b.kb = static_cast<int>((L.F + kBK - 1) / kBK);
-    b.tiles = static_cast<int>((L.d + kDJ * kBM - 1) / (kDJ * kBM)) * p.n_tiles;
+    b.d = static_cast<int>(L.d);
+    b.nkb = static_cast<int>((L.F + kBK - 1) / kBK);
+    b.n_tt = static_cast<int>((nb + kPfM - 1) / kPfM);
+    b.n_jt = static_cast<int>((L.d + kPfN - 1) / kPfN);
+    const int tiles = b.n_tt * b.n_jt;
+    const int dgrid = std::min(c.num_sms, kMaxCtas);
+    b.n_full = tiles / dgrid * dgrid;
     b.y = y;
-    const int dcols = 2 * kDJ * p.nbt;  // double-buffered accumulators
-    b.tmem_cols = dcols <= 32 ? 32 : dcols <= 64 ? 64 : dcols <= 128 ? 128 : dcols <= 256 ? 256 : 512;
-    const int brows = 2 * p.nbt;
-    const int dstage = kDJ * kBM * kBK * 2 + brows * kBK * 2;
-    b.stages = static_cast<int>(std::min<size_t>(8, (kMaxDynSmem - fixed) / dstage));
-    if (st_env > 0) b.stages = std::min(b.stages, st_env);
-    const size_t dsmem = fixed + static_cast<size_t>(b.stages) * dstage;
-    CUtensorMap m_w, m_s;
-    // W_down as [F rows (K), d columns (M)]: boxes of 64 columns x 64 rows
-    if (!make_map(&m_w, L.w_down, L.F, L.d, L.rs, kBK) || !make_map(&m_s, sb, p.rows, L.F, ld_s, brows))
+    b.stages = static_cast<int>(std::min<size_t>(4, (kMaxDynSmem - fixed) / kPfStage));
+    const size_t dsmem = fixed + static_cast<size_t>(b.stages) * kPfStage;
+    CUtensorMap m_s, m_w;
+    if (!make_map(&m_s, sb, p.rows, L.F, ld_s, kBM) || !make_map(&m_w, L.w_down, L.F, L.d, L.rs, kBK))
         return cudaErrorInvalidValue;
-    const int64_t dunits = static_cast<int64_t>(b.tiles) * b.kb;
-    int dgrid = static_cast<int>(std::min<int64_t>(std::min(c.num_sms, kMaxCtas), dunits));
-    if (grid_env > 0 && grid_env < dgrid) dgrid = grid_env;
-    if ((e = set_smem(k_tc_down, dsmem)) != cudaSuccess) return e;
-    k_tc_down<<<dgrid, kThreads, dsmem, c.stream>>>(m_w, m_s, b);
-    return cudaGetLastError();
+    if (tiles > b.n_full) {
+        k_tc_zero_tiles<<<dim3(static_cast<unsigned>(tiles - b.n_full), 8), 256, 0, c.stream>>>(y, b.nb, b.d, b.n_jt,
+                                                                                                  b.n_full);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if ((e = set_smem(k_tc_pf_down, dsmem)) != cudaSuccess) return e;
+    return launch_ex(k_tc_pf_down, dim3(dgrid), dim3(kThreads), dsmem, c, true, m_s, m_w, b);
 }
 
 }  // namespace tc

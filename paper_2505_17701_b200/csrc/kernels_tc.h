@@ -1,7 +1,6 @@
 // kernels_tc.h -- batched decode / prefill on the tensor cores (kernels_tc.cu).
 #pragma once
 
-#include <cublas_v2.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -34,15 +33,6 @@ struct GateUpArgs {
     int* alive_out = nullptr;         // nb
 };
 
-// Arguments of the phase-B kernel (k_tc_down).
-struct DownArgs {
-    int d = 0, nb = 0, nbt = 0, n_tiles = 0;
-    int kb = 0;          // 64-neuron k-blocks
-    int tiles = 0;       // j-tiles x n-tiles
-    int stages = 0, tmem_cols = 0;
-    float* y = nullptr;  // nb x d, zeroed; accumulated with red.add
-};
-
 // Tiling of a batch: `split` carries activations as bf16 (hi, lo) pairs (decode); nbt samples per
 // n-tile; rows = B-operand rows of the whole batch (n_tiles x N).
 struct Plan {
@@ -58,8 +48,7 @@ size_t workspace_bytes(const LayerDev& L, const Plan& p, int num_sms);
 // `ws` holds workspace_bytes(L, p); `flags` kMaxCtas zero-initialised words (left zero);
 // alive_out is zeroed and accumulated.  Returns
 // cudaErrorInvalidValue for layers it does not cover (f32 weights, missing predictor).
-cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned* flags, cublasHandle_t blas,
-                           int method, int64_t nb,
+cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned* flags, int method, int64_t nb,
                            const float* x, float tau, const uint8_t* ovr, float* y, uint8_t* mask_out,
                            float* ind_out, int* alive_out, const LaunchCfg& c);
 

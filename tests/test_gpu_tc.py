@@ -195,3 +195,34 @@ def test_tc_qwen_b64_decode_and_prefill(oracle):
     y = cd.exec_dense(layer, P, FAST)
     for b in (0, 257, 511):
         assert rel_l2(y[b], oracle.forward_dense(g, P[b])["y"]) <= 1e-2
+
+
+@pytest.mark.slow
+def test_tc_prefill_2048_tokens_sampled(oracle):
+    """BASELINE.json config 5 prefill chunk at full size: Qwen2.5-14B FFN, 2048 tokens through the
+    repo's own tcgen05 gate/up and down kernels (whole 256 x 256 tiles on every CTA plus the
+    stream-K remainder), 64 sampled tokens across every token tile vs the oracle's forward_dense
+    (bf16 activations: the north_star 1e-2 bound)."""
+    d, F, r = 5120, 13824, 512
+    g, layer, _ = make(oracle, 42, d, F, r)
+    P = batch(oracle, 79, 2048, d)
+    y = cd.exec_dense(layer, P, FAST)
+    assert layer.device_layer().last_path() == "tensor"
+    rng = np.random.default_rng(5)
+    rows = np.unique(np.concatenate([rng.integers(0, 2048, 56), [0, 255, 256, 1023, 1791, 1792, 2046, 2047]]))
+    assert len(rows) >= 60
+    for b in rows:
+        assert rel_l2(y[b], oracle.forward_dense(g, P[b])["y"]) <= 1e-2, b
+
+
+@pytest.mark.parametrize("shape,B", [((200, 300, 8), 600), ((130, 500, 8), 257), ((512, 1024, 8), 1100)])
+def test_tc_prefill_ragged(oracle, shape, B):
+    """Prefill on ragged shapes: d not a multiple of 4 (scalar epilogue) or of the 256-column tile,
+    F not a multiple of 64 (TMA zero fill along K), partial token tiles."""
+    d, F, r = shape
+    g, layer, _ = make(oracle, 300 + d, d, F, r)
+    X = batch(oracle, 12, B, d)
+    y = cd.exec_dense(layer, X, FAST)
+    assert layer.device_layer().last_path() == "tensor"
+    for b in list(range(0, B, max(1, B // 24))) + [B - 1]:
+        assert rel_l2(y[b], oracle.forward_dense(g, X[b])["y"]) <= 1e-2, b

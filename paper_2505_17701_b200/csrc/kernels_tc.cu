@@ -53,6 +53,18 @@ namespace {
 // (grid <= SMs, one CTA per SM).
 constexpr int kOvr = 4;  // epilogue kind: D-CountDown with a given mask (override / exec_dc)
 
+// Prefill (a.dp): whole tiles instead -- wave w gives CTA c tile w G + c, tiles m-major, so the
+// token tiles of one neuron tile run side by side on neighbouring CTAs and read its weight
+// k-blocks through L2 once (stream-K ranges would re-stream each neuron tile from HBM per
+// token tile: 8x the weight bytes at 2048 tokens).
+__device__ __forceinline__ bool gu_seg(int c, int si, int64_t U, int G, int nkb, bool dp, int tiles, Seg& sg) {
+    if (!dp) return seg_at(c, si, U, G, nkb, sg);
+    const int t = c + si * G;
+    if (t >= tiles) return false;
+    sg = {t, 0, nkb};
+    return true;
+}
+
 template <int KIND, bool SPLIT, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUtensorMap m_gate,
@@ -113,11 +125,13 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
     if (warp == 0) {
         if (lane == 0) {
             // ---- TMA producer: the CTA's k-blocks in order, one continuous ring
-            const uint64_t pw = policy_evict_first();  // weights: streamed once
-            const uint64_t px = policy_evict_last();   // activations: re-read by every neuron tile
+            // weights: streamed once (decode) / shared by the token tiles of a wave (prefill);
+            // activations: re-read by every neuron tile
+            const uint64_t pw = a.dp ? policy_evict_last() : policy_evict_first();
+            const uint64_t px = policy_evict_last();
             int it = 0;
             Seg sg;
-            for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+            for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg); ++si) {
                 const int m0 = (sg.tile / a.n_tiles) * kBM;
                 const int row0 = (sg.tile % a.n_tiles) * N;
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
@@ -146,7 +160,7 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
             const uint32_t tU = tmem, tG = tmem + N, tZ = tmem + 2 * N;
             int it = 0;
             Seg sg;
-            for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+            for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg); ++si) {
                 if (si > 0) {
                     mbar_wait(tempty, (si - 1) & 1);  // the epilogue drained the previous segment
                     tc_fence_after();
@@ -190,7 +204,7 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
         constexpr int kH = SPLIT ? 2 : 1;
         constexpr int kC = 8;  // samples per chunk
         Seg sg;
-        for (int si = 0; seg_at(c, si, U, G, nkb, sg); ++si) {
+        for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg); ++si) {
             mbar_wait(tfull, si & 1);
             tc_fence_after();
             if (et == 0) stamp(3 + (si > 2 ? 2 : si));
@@ -229,7 +243,7 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
             const int tile = sg.tile;
             const int64_t tile_base = static_cast<int64_t>(tile) * nkb;
             int c_last = c;
-            while (c_last + 1 < G && range_lo(c_last + 1, U, G) < tile_base + nkb) ++c_last;
+            while (!a.dp && c_last + 1 < G && range_lo(c_last + 1, U, G) < tile_base + nkb) ++c_last;
             // the contributors' partials, pulled into the (now idle) ring with bulk copies when
             // they fit -- the finisher segment is its CTA's last, so no stage is in flight
             const int64_t slot_floats = static_cast<int64_t>(kParts) * a.nbt * kBM;
@@ -690,6 +704,7 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     a.tiles = static_cast<int>((L.F + kBM - 1) / kBM) * p.n_tiles;
     const int64_t units = static_cast<int64_t>(a.tiles) * a.kb_x;
     a.tl = nullptr;
+    a.dp = 1;
     const int grid = static_cast<int>(std::min<int64_t>(std::min(c.num_sms, kMaxCtas), units));
     a.ws = ws_partial;
     a.flags = flags;

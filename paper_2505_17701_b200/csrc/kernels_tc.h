@@ -21,6 +21,7 @@ struct GateUpArgs {
     int tmem_cols = 0;
     int tiles = 0;      // m-tiles x n-tiles
     int n_tiles = 0;
+    int dp = 0;                 // whole tiles in waves (prefill) instead of stream-K ranges
     float* ws = nullptr;        // stream-K partial accumulators, one slot per CTA
     unsigned* flags = nullptr;  // one release flag per CTA (zero between launches)
     unsigned long long* tl = nullptr;  // development: per-CTA globaltimer stamps (8 per CTA) or null

@@ -314,9 +314,9 @@ int run_chain(cd_layer* h, const Req& r) {
         h->last_path = CD_PATH_TENSOR;
         if (p.split) return 1;  // decode: one persistent kernel (k_tc_fused)
         // prefill: x pack, gate/up, [zero of the stream-K tiles], down
-        const int64_t tiles = ((r.nb + 255) / 256) * ((d + 255) / 256);
-        const int64_t grid = std::min<int64_t>(c.num_sms, cdk::kMaxCtas);
-        return 3 + (tiles % grid != 0 ? 1 : 0);
+        const int64_t units = ((r.nb + 255) / 256) * ((d + 511) / 512);  // column-tile pairs
+        const int64_t clusters = (std::min<int64_t>(c.num_sms, cdk::kMaxCtas) & ~1) / 2;
+        return 3 + (units % clusters != 0 ? 1 : 0);
     }
     h->last_path = r.reduction == CD_REDUCTION_UNORDERED ? CD_PATH_FAST : CD_PATH_EXACT;
     if (r.reduction == CD_REDUCTION_UNORDERED) {

@@ -57,8 +57,21 @@ constexpr int kOvr = 4;  // epilogue kind: D-CountDown with a given mask (overri
 // token tiles of one neuron tile run side by side on neighbouring CTAs and read its weight
 // k-blocks through L2 once (stream-K ranges would re-stream each neuron tile from HBM per
 // token tile: 8x the weight bytes at 2048 tokens).
-__device__ __forceinline__ bool gu_seg(int c, int si, int64_t U, int G, int nkb, bool dp, int tiles, Seg& sg) {
+// With a 2-CTA cluster (mc), the two CTAs of a cluster take the two token tiles of one
+// (neuron tile, token-tile pair) and each multicasts one of the two weight boxes to both: the
+// tile index is then m ntp + tt with ntp the token-tile count rounded up to even (a phantom
+// odd tile reads zero-filled rows and stores nothing).
+__device__ __forceinline__ bool gu_seg(int c, int si, int64_t U, int G, int nkb, bool dp, int tiles, Seg& sg,
+                                       int mc = 0, int n_tiles = 1) {
     if (!dp) return seg_at(c, si, U, G, nkb, sg);
+    if (mc) {
+        const int half = (n_tiles + 1) / 2;  // token-tile pairs per neuron tile
+        const int pairs = (tiles / n_tiles) * half;
+        const int pi = (c >> 1) + si * (G >> 1);
+        if (pi >= pairs) return false;
+        sg = {(pi / half) * 2 * half + 2 * (pi % half) + (c & 1), 0, nkb};
+        return true;
+    }
     const int t = c + si * G;
     if (t >= tiles) return false;
     sg = {t, 0, nkb};
@@ -76,9 +89,13 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
     const int stage_bytes = 2 * kABytes + N * kBK * 2;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
     uint64_t* empty = full + a.stages;
-    uint64_t* tfull = empty + a.stages;  // accumulators of a segment complete (MMA -> epilogue)
-    uint64_t* tempty = tfull + 1;        // accumulators drained (epilogue -> MMA)
-    uint64_t* pbar = tempty + 1;         // contributor partials landed in smem (finisher)
+    uint64_t* tfull = empty + a.stages;  // [2] accumulators of a segment complete (MMA -> epilogue)
+    uint64_t* tempty = tfull + 2;        // [2] accumulators drained (epilogue -> MMA)
+    uint64_t* pbar = tempty + 2;         // contributor partials landed in smem (finisher)
+    // TMEM buffers: segment si accumulates into buffer si % nbuf (columns [b bstride, ...)), so
+    // with two buffers the epilogue of one tile overlaps the MMAs of the next
+    const int nbuf = a.nbuf > 1 ? 2 : 1;
+    const uint32_t bstride = static_cast<uint32_t>(a.buf_cols);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -89,10 +106,12 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
+            mbar_init(empty + s, a.mc ? 2 : 1);  // mc: both CTAs' MMAs read the multicast boxes
         }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, kEpiThreads);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull + b, 1);
+            mbar_init(tempty + b, kEpiThreads);
+        }
         mbar_init(pbar, 1);
         fence_mbar_init();
         prefetch_map(&m_up);
@@ -111,8 +130,10 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
     }
     tc_fence_before();
     __syncthreads();
+    if (a.mc) cluster_sync();  // the peer's barriers are initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const int ntd = a.mc ? (a.n_tiles + 1) & ~1 : a.n_tiles;  // token tiles per neuron tile (decode)
     auto stamp = [&](int k) {
         if (a.tl) {
             unsigned long long t;
@@ -131,9 +152,9 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
             const uint64_t px = policy_evict_last();
             int it = 0;
             Seg sg;
-            for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg); ++si) {
-                const int m0 = (sg.tile / a.n_tiles) * kBM;
-                const int row0 = (sg.tile % a.n_tiles) * N;
+            for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg, a.mc, a.n_tiles); ++si) {
+                const int m0 = (sg.tile / ntd) * kBM;
+                const int row0 = (sg.tile % ntd) * N;
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
                     const int s = it % a.stages;
                     if (it >= a.stages) mbar_wait(empty + s, ((it / a.stages) - 1) & 1);
@@ -146,8 +167,14 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
                         const int k = (kb - a.kb_z) * kBK;
                         if (it == 0) stamp(1);
                         mbar_arrive_expect_tx(full + s, 2 * kABytes + N * kBK * 2);
-                        tma_load_2d(st, &m_up, k, m0, full + s, pw);
-                        tma_load_2d(st + kABytes, &m_gate, k, m0, full + s, pw);
+                        if (!a.mc) {
+                            tma_load_2d(st, &m_up, k, m0, full + s, pw);
+                            tma_load_2d(st + kABytes, &m_gate, k, m0, full + s, pw);
+                        } else if ((c & 1) == 0) {
+                            tma_load_2d_mc(st, &m_up, k, m0, full + s, 0x3, pw);
+                        } else {
+                            tma_load_2d_mc(st + kABytes, &m_gate, k, m0, full + s, 0x3, pw);
+                        }
                         tma_load_2d(st + 2 * kABytes, &m_x, k, row0, full + s, px);
                     }
                 }
@@ -157,14 +184,15 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
         if (lane == 0) {
             // ---- MMA issuer: U at TMEM columns [0, N), G at [N, 2N), Z at [2N, 3N)
             const uint32_t idesc = idesc_bf16(kBM, N);
-            const uint32_t tU = tmem, tG = tmem + N, tZ = tmem + 2 * N;
             int it = 0;
             Seg sg;
-            for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg); ++si) {
-                if (si > 0) {
-                    mbar_wait(tempty, (si - 1) & 1);  // the epilogue drained the previous segment
+            for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg, a.mc, a.n_tiles); ++si) {
+                const int bf = si % nbuf;
+                if (si >= nbuf) {
+                    mbar_wait(tempty + bf, ((si / nbuf) - 1) & 1);  // the epilogue drained this buffer
                     tc_fence_after();
                 }
+                const uint32_t tU = tmem + bf * bstride, tG = tU + N, tZ = tU + 2 * N;
                 const int first_ug = max(sg.kb0, a.kb_z);
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
                     const int s = it % a.stages;
@@ -185,9 +213,11 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
                             umma_bf16(tG, da1 + o, db + o, idesc, acc);
                         }
                     }
-                    umma_commit(empty + s);  // frees the stage once these MMAs have read it
+                    // frees the stage once these MMAs have read it (mc: in both CTAs)
+                    if (a.mc) umma_commit_mc(empty + s, 0x3);
+                    else umma_commit(empty + s);
                 }
-                umma_commit(tfull);
+                umma_commit(tfull + bf);
             }
             stamp(2);
         }
@@ -198,15 +228,17 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
         const int half = (warp - 2) >> 2;
         const int m = g * 32 + lane;
         const int et = threadIdx.x - 64;  // 0 .. kEpiThreads-1
-        const uint32_t trow = tmem + (static_cast<uint32_t>(g * 32) << 16);
+        const uint32_t trow0 = tmem + (static_cast<uint32_t>(g * 32) << 16);
         constexpr bool kZ = KIND == kDC;
         constexpr int kParts = kZ ? 3 : 2;
         constexpr int kH = SPLIT ? 2 : 1;
         constexpr int kC = 8;  // samples per chunk
         Seg sg;
-        for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg); ++si) {
-            mbar_wait(tfull, si & 1);
+        for (int si = 0; gu_seg(c, si, U, G, nkb, a.dp != 0, a.tiles, sg, a.mc, a.n_tiles); ++si) {
+            const int bf = si % nbuf;
+            mbar_wait(tfull + bf, (si / nbuf) & 1);
             tc_fence_after();
+            const uint32_t trow = trow0 + bf * bstride;
             if (et == 0) stamp(3 + (si > 2 ? 2 : si));
             const bool has_z = kZ && sg.kb0 < a.kb_z;
             const bool has_ug = sg.kb1 > a.kb_z;
@@ -233,7 +265,7 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(tempty);
+                mbar_arrive(tempty + bf);
                 __threadfence();
                 named_bar_sync(1, kEpiThreads);
                 if (et == 0) st_release_u32(a.flags + c, 1u);
@@ -269,8 +301,8 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
                     mbar_wait(pbar, 0);
                 }
             }
-            const int m0 = (tile / a.n_tiles) * kBM;
-            const int ntile = tile % a.n_tiles;
+            const int m0 = (tile / ntd) * kBM;
+            const int ntile = tile % ntd;
             const int i = m0 + m;
             const bool valid = i < a.F;
             const int nbt = a.nbt;
@@ -369,12 +401,13 @@ k_tc_gateup(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CU
                 }
             }
             tc_fence_before();
-            mbar_arrive(tempty);
+            mbar_arrive(tempty + bf);
         }
         tc_fence_before();
         if (et == 0) stamp(6);
     }
     __syncthreads();
+    if (a.mc) cluster_sync();  // no multicast or remote commit still targets this CTA
     if (threadIdx.x == 0) stamp(7);
     if (warp == 1) {
         tc_fence_after();
@@ -404,8 +437,10 @@ struct PfDownArgs {
     int nb = 0, d = 0;
     int nkb = 0;            // 64-neuron k-blocks
     int n_tt = 0, n_jt = 0; // token tiles, column tiles
-    int n_full = 0;         // tiles done whole (a multiple of the grid), the rest stream-K
+    int n_full = 0;         // (pair-)tiles done whole (a multiple of the grid), the rest stream-K
     int stages = 0;
+    int mc = 0;             // 2-CTA clusters: the pair takes two column tiles of one token tile and
+                            // each CTA multicasts one of the two S boxes to both
     float* y = nullptr;
 };
 
@@ -417,16 +452,27 @@ struct PfSeg {
 // Segment si of CTA c: its whole tiles c, c + G, ... < n_full, then its stream-K range over the
 // remaining tiles' k-blocks.
 __device__ __forceinline__ bool pf_seg(int c, int si, int G, const PfDownArgs& a, PfSeg& sg) {
-    const int n_whole = a.n_full > c ? (a.n_full - c + G - 1) / G : 0;
+    // units of the schedule: tiles, or (mc) column-tile pairs handled by the CTA pairs
+    const int ju = a.mc ? (a.n_jt + 1) / 2 : a.n_jt;
+    const int units = a.n_tt * ju;
+    const int w = a.mc ? c >> 1 : c;
+    const int W = a.mc ? G >> 1 : G;
+    int u = -1, kb0 = 0, kb1 = a.nkb;
+    bool whole = false;
+    const int n_whole = a.n_full > w ? (a.n_full - w + W - 1) / W : 0;
     if (si < n_whole) {
-        sg = {c + si * G, 0, a.nkb, true};
-        return true;
+        u = w + si * W;
+        whole = true;
+    } else {
+        const int64_t U = static_cast<int64_t>(units - a.n_full) * a.nkb;
+        Seg s2;
+        if (U <= 0 || !seg_at(w, si - n_whole, U, W, a.nkb, s2)) return false;
+        u = a.n_full + s2.tile;
+        kb0 = s2.kb0;
+        kb1 = s2.kb1;
     }
-    const int tiles = a.n_tt * a.n_jt;
-    const int64_t U = static_cast<int64_t>(tiles - a.n_full) * a.nkb;
-    Seg s2;
-    if (U <= 0 || !seg_at(c, si - n_whole, U, G, a.nkb, s2)) return false;
-    sg = {a.n_full + s2.tile, s2.kb0, s2.kb1, false};
+    const int tt = u / ju, jt = a.mc ? 2 * (u % ju) + (c & 1) : u % ju;
+    sg = {tt * (a.mc ? 2 * ju : a.n_jt) + jt, kb0, kb1, whole};
     return true;
 }
 
@@ -441,11 +487,12 @@ k_tc_pf_down(const __grid_constant__ CUtensorMap m_s, const __grid_constant__ CU
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, c = blockIdx.x;
+    const int jw = a.mc ? 2 * ((a.n_jt + 1) / 2) : a.n_jt;  // tile index = tt jw + jt
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < a.stages; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
+            mbar_init(empty + s, a.mc ? 2 : 1);
         }
         mbar_init(tfull, 1);
         mbar_init(tempty, kEpiThreads);
@@ -461,6 +508,7 @@ k_tc_pf_down(const __grid_constant__ CUtensorMap m_s, const __grid_constant__ CU
     }
     tc_fence_before();
     __syncthreads();
+    if (a.mc) cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_wait();  // S comes from the gate/up kernel
@@ -472,14 +520,19 @@ k_tc_pf_down(const __grid_constant__ CUtensorMap m_s, const __grid_constant__ CU
             int it = 0;
             PfSeg sg;
             for (int si = 0; pf_seg(c, si, G, a, sg); ++si) {
-                const int tt = sg.tile / a.n_jt, jt = sg.tile % a.n_jt;
+                const int tt = sg.tile / jw, jt = sg.tile % jw;
                 for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
                     const int s = it % a.stages;
                     if (it >= a.stages) mbar_wait(empty + s, ((it / a.stages) - 1) & 1);
                     uint8_t* st = smem + s * kPfStage;
                     mbar_arrive_expect_tx(full + s, kPfStage);
-                    tma_load_2d(st, &m_s, kb * kBK, tt * kPfM, full + s, ps);
-                    tma_load_2d(st + kABytes, &m_s, kb * kBK, tt * kPfM + kBM, full + s, ps);
+                    if (!a.mc) {
+                        tma_load_2d(st, &m_s, kb * kBK, tt * kPfM, full + s, ps);
+                        tma_load_2d(st + kABytes, &m_s, kb * kBK, tt * kPfM + kBM, full + s, ps);
+                    } else {
+                        const int h = c & 1;  // this CTA's half of the shared S boxes
+                        tma_load_2d_mc(st + h * kABytes, &m_s, kb * kBK, tt * kPfM + h * kBM, full + s, 0x3, ps);
+                    }
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
                         tma_load_2d(st + 2 * kABytes + q * (kBK * kBK * 2), &m_w, jt * kPfN + 64 * q, kb * kBK,
@@ -514,7 +567,8 @@ k_tc_pf_down(const __grid_constant__ CUtensorMap m_s, const __grid_constant__ CU
                                       idesc, (kb > sg.kb0 || k > 0) ? 1u : 0u);
                         }
                     }
-                    umma_commit(empty + s);
+                    if (a.mc) umma_commit_mc(empty + s, 0x3);
+                    else umma_commit(empty + s);
                 }
                 umma_commit(tfull);
             }
@@ -528,7 +582,7 @@ k_tc_pf_down(const __grid_constant__ CUtensorMap m_s, const __grid_constant__ CU
         for (int si = 0; pf_seg(c, si, G, a, sg); ++si) {
             mbar_wait(tfull, si & 1);
             tc_fence_after();
-            const int tt = sg.tile / a.n_jt, jt = sg.tile % a.n_jt;
+            const int tt = sg.tile / jw, jt = sg.tile % jw;
             const int64_t tok = static_cast<int64_t>(tt) * kPfM + h * kBM + g * 32 + lane;
             float* yrow = a.y + tok * a.d + jt * kPfN;
             const bool row_ok = tok < a.nb;
@@ -562,16 +616,21 @@ k_tc_pf_down(const __grid_constant__ CUtensorMap m_s, const __grid_constant__ CU
         }
     }
     __syncthreads();
+    if (a.mc) cluster_sync();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
     }
 }
 
-// Zero the stream-K tiles' blocks of y (tile-major from `first`): grid (tiles, 256 / 8) x 256 threads.
-__global__ void k_tc_zero_tiles(float* __restrict__ y, int nb, int d, int n_jt, int first) {
-    const int t = first + blockIdx.x;
-    const int tt = t / n_jt, jt = t % n_jt;
+// Zero the blocks of y of the stream-K units >= first (tiles, or mc column-tile pairs):
+// grid (units x 2, 8) x 256 threads.
+__global__ void k_tc_zero_tiles(float* __restrict__ y, int nb, int d, int n_jt, int first, int mc) {
+    const int ju = mc ? (n_jt + 1) / 2 : n_jt;
+    const int u = first + blockIdx.x / 2;
+    const int tt = u / ju;
+    const int jt = mc ? 2 * (u % ju) + (blockIdx.x & 1) : u % ju;
+    if ((!mc && (blockIdx.x & 1)) || jt >= n_jt) return;
     const int c0 = jt * kPfN, ncols = min(kPfN, d - c0);
     for (int r = blockIdx.y * 8 + threadIdx.x / 32; r < kPfM; r += gridDim.y * 8) {
         const int64_t tok = static_cast<int64_t>(tt) * kPfM + r;
@@ -624,7 +683,9 @@ int64_t round_up64(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 Plan plan_for(int64_t nb, int method) {
     Plan p;
     // Decode: pairs of bf16 (hi, lo) per activation, up to 64 samples per n-tile (UMMA N = 128).
-    // Large dense batches (prefill): single bf16 activations, 256 tokens per n-tile.
+    // Large dense batches (prefill): single bf16 activations, 256 tokens per n-tile (U and G fill
+    // the 512 TMEM columns; N = 128 with double-buffered accumulators measured 1.5x slower: the
+    // two MMAs per k-step then read 2 x 4 KB of B per 64 cycles, past the shared-memory port).
     p.split = !(method == kDense && nb > 256);
     if (p.split) {
         p.nbt = static_cast<int>(std::min<int64_t>(64, round_up64(nb, 16)));  // epilogue chunks of 16
@@ -702,10 +763,10 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     if (2 * p.N > 512) return cudaErrorInvalidValue;
     a.n_tiles = p.n_tiles;
     a.tiles = static_cast<int>((L.F + kBM - 1) / kBM) * p.n_tiles;
-    const int64_t units = static_cast<int64_t>(a.tiles) * a.kb_x;
     a.tl = nullptr;
     a.dp = 1;
-    const int grid = static_cast<int>(std::min<int64_t>(std::min(c.num_sms, kMaxCtas), units));
+    a.mc = 1;
+    const int grid = std::min(c.num_sms, kMaxCtas) & ~1;  // pairs of CTAs (2-CTA clusters)
     a.ws = ws_partial;
     a.flags = flags;
     const int stage_bytes = 2 * kABytes + p.N * kBK * 2;
@@ -715,8 +776,9 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     auto fn = L.act == 0 ? k_tc_gateup<kDense, false, 0> : k_tc_gateup<kDense, false, 1>;
     if ((e = set_smem(fn, smem)) != cudaSuccess) return e;
     CUtensorMap m_tb = m_up, m_lat = m_x;
-    fn<<<grid, kThreads, smem, c.stream>>>(m_up, m_gate, m_x, m_tb, m_lat, a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_ex_cluster(fn, dim3(grid), dim3(kThreads), smem, c, false, 2u, m_up, m_gate, m_x, m_tb, m_lat,
+                               a)) != cudaSuccess)
+        return e;
 
     // y = s W_down (W_down rows are the third part of each neuron record, stride rs)
     PfDownArgs b;
@@ -725,22 +787,24 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     b.nkb = static_cast<int>((L.F + kBK - 1) / kBK);
     b.n_tt = static_cast<int>((nb + kPfM - 1) / kPfM);
     b.n_jt = static_cast<int>((L.d + kPfN - 1) / kPfN);
-    const int tiles = b.n_tt * b.n_jt;
-    const int dgrid = std::min(c.num_sms, kMaxCtas);
-    b.n_full = tiles / dgrid * dgrid;
+    const int dgrid = std::min(c.num_sms, kMaxCtas) & ~1;
+    b.mc = 1;
+    const int W = dgrid / 2;
+    const int dunits = b.n_tt * ((b.n_jt + 1) / 2);
+    b.n_full = dunits / W * W;
     b.y = y;
     b.stages = static_cast<int>(std::min<size_t>(4, (kMaxDynSmem - fixed) / kPfStage));
     const size_t dsmem = fixed + static_cast<size_t>(b.stages) * kPfStage;
     CUtensorMap m_s, m_w;
     if (!make_map(&m_s, sb, p.rows, L.F, ld_s, kBM) || !make_map(&m_w, L.w_down, L.F, L.d, L.rs, kBK))
         return cudaErrorInvalidValue;
-    if (tiles > b.n_full) {
-        k_tc_zero_tiles<<<dim3(static_cast<unsigned>(tiles - b.n_full), 8), 256, 0, c.stream>>>(y, b.nb, b.d, b.n_jt,
-                                                                                                  b.n_full);
+    if (dunits > b.n_full) {
+        k_tc_zero_tiles<<<dim3(static_cast<unsigned>(2 * (dunits - b.n_full)), 8), 256, 0, c.stream>>>(
+            y, b.nb, b.d, b.n_jt, b.n_full, b.mc);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if ((e = set_smem(k_tc_pf_down, dsmem)) != cudaSuccess) return e;
-    return launch_ex(k_tc_pf_down, dim3(dgrid), dim3(kThreads), dsmem, c, true, m_s, m_w, b);
+    return launch_ex_cluster(k_tc_pf_down, dim3(dgrid), dim3(kThreads), dsmem, c, true, 2u, m_s, m_w, b);
 }
 
 }  // namespace tc

@@ -22,6 +22,8 @@ struct GateUpArgs {
     int tiles = 0;      // m-tiles x n-tiles
     int n_tiles = 0;
     int dp = 0;                 // whole tiles in waves (prefill) instead of stream-K ranges
+    int mc = 0;                 // dp with 2-CTA clusters multicasting the weight boxes
+    int nbuf = 1, buf_cols = 0; // TMEM accumulator buffers and columns per buffer
     float* ws = nullptr;        // stream-K partial accumulators, one slot per CTA
     unsigned* flags = nullptr;  // one release flag per CTA (zero between launches)
     unsigned long long* tl = nullptr;  // development: per-CTA globaltimer stamps (8 per CTA) or null

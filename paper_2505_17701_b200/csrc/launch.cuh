@@ -46,6 +46,32 @@ cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, const Launch
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// The same with a cluster of `cluster_x` CTAs (grid.x a multiple of it).
+template <typename K, typename... Args>
+cudaError_t launch_ex_cluster(K kernel, dim3 grid, dim3 block, size_t smem, const LaunchCfg& c, bool pdl_attr,
+                              unsigned cluster_x, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+    if (pdl_attr && c.pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Opt the kernel into all the dynamic shared memory it can get (device opt-in limit minus the
 // kernel's static shared memory) once per process; cached, so the per-call host cost is a hash
 // lookup and the call is safe during graph capture.  Fails if `bytes` does not fit.

@@ -121,3 +121,31 @@ def test_properties_at_full_size(oracle, llama):
     part = rng.integers(0, 3, F)
     ys = [cd.exec_dc(layer, x, (part == p).astype(np.uint8), FAST).astype(np.float64) for p in range(3)]
     assert rel_l2(sum(ys), dense) <= 1e-5
+
+
+@pytest.mark.parametrize("B", [1, 16])
+def test_gemma_b1_b16_dc_mc(oracle, B):
+    """BASELINE configs[2] at batch 1 (fused CUDA-core kernels) and 16 (tensor-core path):
+    Gemma-2-9B FFN (3584 x 14336, GeLU-tanh), D- and M-CountDown at ~90%, per-sample masks."""
+    d, F, r = 3584, 14336, 512
+    g = oracle.generate(11, d, F, r)
+    g = {k: bf16_round(v) for k, v in g.items()}
+    layer = cd.GatedMlpLayer(d, F, 1, g["w_up"], g["w_gate"], g["w_down"], device_dtype="bf16")
+    pred = cd.Predictor(cd.LowRankPredictor(d, r, F, g["theta_a"], g["theta_b"]), "bf16")
+    X = np.stack([cd.synth_normals(3000 + i, d) for i in range(B)])
+    zs = [oracle.lowrank_logits(g["theta_a"], g["theta_b"], x)[1] for x in X]
+    tau = float(np.mean([np.quantile(z, 0.9) for z in zs]))
+    res = cd.pipeline_dc(layer, X if B > 1 else X[0], pred, FAST, tau_d=tau)
+    masks = res.mask if B > 1 else [res.mask]
+    ys = res.y if B > 1 else [res.y]
+    assert layer.device_layer(pred).last_path() == ("tensor" if B >= 8 else "fast")
+    for b in range(B):
+        assert rel_l2(ys[b], oracle.forward_sparse(g, X[b], masks[b].alive, act=1)) <= 1e-4
+        assert 0.85 <= 1 - masks[b].alive_count / F <= 0.95
+    us = [np.abs(oracle.gemv(g["w_up"], x)) for x in X]
+    tau_u = float(np.mean([np.quantile(u, 0.9) for u in us]))
+    res = cd.pipeline_mc(layer, X if B > 1 else X[0], tau_u, FAST)
+    masks = res.mask if B > 1 else [res.mask]
+    ys = res.y if B > 1 else [res.y]
+    for b in range(B):
+        assert rel_l2(ys[b], oracle.forward_sparse(g, X[b], masks[b].alive, act=1)) <= 1e-4

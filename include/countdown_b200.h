@@ -131,11 +131,17 @@ CD_API int cd_layer_last_path(const cd_layer* h, int* path);
  * the multi-kernel chains).  CD_ENGINE_TENSOR: bf16 layers at batch >= 8 on the tcgen05
  * masked row-union GEMM (off: the CUDA-core kernels in chunks of 4).  CD_ENGINE_HOST_GRAPH:
  * host-buffer calls replay a captured CUDA graph of their whole sequence.  Results stay
- * within each reduction mode's contract whatever the selection; this is for A/B tests. */
+ * within each reduction mode's contract whatever the selection; this is for A/B tests.
+ * CD_ENGINE_PDL_CHAIN (off by default): the batch-1..4 persistent kernels (k_dc_fused,
+ * k_mc_fused) are launched with programmatic dependent launch instead of as cooperative
+ * grids, so a step's prologue overlaps the previous step's tail (1.4 us per Llama-shape step
+ * measured).  The caller then guarantees that no other kernel shares the device while these
+ * run (their CTAs wait on each other; a cooperative launch makes the driver guarantee it). */
 #define CD_ENGINE_FUSED 1
 #define CD_ENGINE_TENSOR 2
 #define CD_ENGINE_HOST_GRAPH 4
 #define CD_ENGINE_ALL 7
+#define CD_ENGINE_PDL_CHAIN 8
 CD_API int cd_layer_set_engines(cd_layer* h, int engines);
 
 /* ---------------------------------------------------------------- host-buffer operators

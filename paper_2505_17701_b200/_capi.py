@@ -20,7 +20,7 @@ ACT_SILU, ACT_GELU_TANH = 0, 1
 DTYPE_F32, DTYPE_BF16 = 0, 1
 REDUCTION_ORDERED, REDUCTION_UNORDERED = 0, 1
 METHOD_DENSE, METHOD_MC, METHOD_DC, METHOD_CATS = 0, 1, 2, 3
-ENGINE_FUSED, ENGINE_TENSOR, ENGINE_HOST_GRAPH, ENGINE_ALL = 1, 2, 4, 7
+ENGINE_FUSED, ENGINE_TENSOR, ENGINE_HOST_GRAPH, ENGINE_ALL, ENGINE_PDL_CHAIN = 1, 2, 4, 7, 8
 
 
 class DataError(RuntimeError):

@@ -388,11 +388,14 @@ class DeviceLayer:
         predictor of `nxt` (the layer that runs next; same shape), or nothing for None."""
         check(lib().cd_layer_set_prefetch(self.raw, None if nxt is None else nxt.raw))
 
-    def set_engines(self, fused: bool = True, tensor: bool = True, host_graph: bool = True) -> None:
+    def set_engines(self, fused: bool = True, tensor: bool = True, host_graph: bool = True,
+                    pdl_chain: bool = False) -> None:
         """cd_layer_set_engines: pick the engines this handle may use (A/B tests; all on by
-        default).  Results stay within each reduction mode's contract whatever the choice."""
+        default).  Results stay within each reduction mode's contract whatever the choice.
+        pdl_chain: the caller owns the device (no concurrent kernels), so the batch-1..4
+        persistent kernels may be PDL-chained instead of launched cooperative."""
         flags = ((_capi.ENGINE_FUSED if fused else 0) | (_capi.ENGINE_TENSOR if tensor else 0) |
-                 (_capi.ENGINE_HOST_GRAPH if host_graph else 0))
+                 (_capi.ENGINE_HOST_GRAPH if host_graph else 0) | (_capi.ENGINE_PDL_CHAIN if pdl_chain else 0))
         check(lib().cd_layer_set_engines(self.raw, flags))
 
     @staticmethod

@@ -105,6 +105,7 @@ struct cd_layer {
     int last_path = CD_PATH_FAST;
     // engines (cd_layer_set_engines): all on by default
     bool use_fused = true;  // batch <= 4 DC / MC as one persistent kernel (off: the kernel chains)
+    bool pdl_chain = false; // CD_ENGINE_PDL_CHAIN: persistent kernels PDL-chained, not cooperative
     bool use_tc = true;     // batches >= kTcMinBatch of a bf16 layer on the tensor cores
     bool weights_finite = true;  // every uploaded weight finite: the row-union GEMM may read any row
     const void* pf_at = nullptr;  // cd_layer_set_prefetch: the next layer's predictor (L2 prefetch)
@@ -280,6 +281,7 @@ int run_chain(cd_layer* h, const Req& r) {
     cdk::LaunchCfg c;
     c.num_sms = h->num_sms;
     c.stream = r.stream ? r.stream : h->stream;
+    c.coop = !h->pdl_chain;
     const int64_t d = L.d, F = L.F;
     int launches = 0;
     if (r.marks) {
@@ -1548,10 +1550,11 @@ CD_API int cd_debug_timeline(unsigned long long* out, int64_t n) {
 int cd_layer_set_engines(cd_layer* h, int engines) {
     return guarded([&] {
         check_layer(h);
-        if (engines & ~(CD_ENGINE_FUSED | CD_ENGINE_TENSOR | CD_ENGINE_HOST_GRAPH))
+        if (engines & ~(CD_ENGINE_FUSED | CD_ENGINE_TENSOR | CD_ENGINE_HOST_GRAPH | CD_ENGINE_PDL_CHAIN))
             fail(CD_ERR_DATA, "set_engines: unknown engine flag");
         CallLock lk(h);
         h->use_fused = (engines & CD_ENGINE_FUSED) != 0;
+        h->pdl_chain = (engines & CD_ENGINE_PDL_CHAIN) != 0;
         h->use_tc = (engines & CD_ENGINE_TENSOR) != 0;
         h->use_host_graph = (engines & CD_ENGINE_HOST_GRAPH) != 0;
         if (h->hg.exec) {

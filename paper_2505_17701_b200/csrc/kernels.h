@@ -69,6 +69,7 @@ struct LaunchCfg {
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     bool pdl = true;
+    bool coop = true;  // persistent kernels: cooperative launch (false: PDL-chained, device owned)
 };
 
 // Indicator kinds

@@ -1100,7 +1100,7 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
         p.n_dot = n_dot;
         p.lat_rep = 1;
         while (p.lat_rep < CD_LAT_REP && (int64_t)p.lat_rep * 2 * nbk * L.ldr <= kMaxBatchFast * 2048) p.lat_rep *= 2;
-        return launch_ex(kern, dim3(G), dim3(threads), smem, c, true, p);
+        return launch_persistent(kern, dim3(G), dim3(threads), smem, c, true, p);
     };
 #define CD_FUSED_CASES(W)                                          \
     switch (nbk * 100 + vpt * 10 + vpl) {                          \

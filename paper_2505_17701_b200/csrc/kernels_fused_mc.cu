@@ -509,7 +509,7 @@ cudaError_t launch_mc_fused(const LayerDev& L, const Scratch& S, const float* x,
 #endif
     }();
         p.tl = tl_env;
-        return launch_ex(kern, dim3(G), dim3(threads), smem, c, true, p);
+        return launch_persistent(kern, dim3(G), dim3(threads), smem, c, true, p);
     };
     if (L.dtype == kBF16) {
         if (vpt == 1) return go(k_mc_fused<__nv_bfloat16, 1>);

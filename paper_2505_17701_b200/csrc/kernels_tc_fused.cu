@@ -697,7 +697,11 @@ cudaError_t launch_batched_fused(const LayerDev& L, const Plan& p, void* ws_base
 #undef CD_TCF_PICK
     if (!fn) return cudaErrorInvalidValue;
     if ((e = set_smem(fn, smem)) != cudaSuccess) return e;
-    fn<<<G, kThreadsF, smem, c.stream>>>(m_up, m_gate, m_x, m_tb, m_lat, m_ta, m_w, m_s, a);
+    LaunchCfg cc = c;
+    cc.coop = true;  // not PDL-chained: the cooperative guarantee costs nothing here
+    if ((e = launch_persistent(fn, dim3(G), dim3(kThreadsF), smem, cc, false, m_up, m_gate, m_x, m_tb, m_lat, m_ta,
+                               m_w, m_s, a)) != cudaSuccess)
+        return e;
     return cudaGetLastError();
 }
 

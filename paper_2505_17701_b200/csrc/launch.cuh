@@ -27,6 +27,7 @@ inline int dev_knob(const char* name, int dflt) {
 
 constexpr size_t kMaxDynSmem = 227 * 1024;
 
+
 // Launch `kernel` on c.stream.  pdl_attr marks the launch as programmatically dependent on
 // the previous kernel in the stream: its CTAs may start while that kernel drains, and must
 // call griddepcontrol.wait before touching anything it produced.
@@ -43,6 +44,35 @@ cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, const Launch
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = (pdl_attr && c.pdl) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// Persistent kernels (one CTA per SM whose CTAs wait on each other's tagged words): launched
+// COOPERATIVE (c.coop), so the driver either makes every CTA co-resident or fails the launch --
+// a kernel resident on another stream (an NCCL communicator, another process under MPS) can
+// then not leave part of the grid unscheduled while the rest spins on it.  c.coop false (the
+// caller owns the device, CD_ENGINE_PDL_CHAIN): programmatic dependent launch as launch_ex.
+template <typename K, typename... Args>
+cudaError_t launch_persistent(K kernel, dim3 grid, dim3 block, size_t smem, const LaunchCfg& c, bool pdl_attr,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (c.coop) {
+        attr[n].id = cudaLaunchAttributeCooperative;
+        attr[n].val.cooperative = 1;
+        ++n;
+    } else if (pdl_attr && c.pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 

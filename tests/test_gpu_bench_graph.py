@@ -17,7 +17,8 @@ from conftest import bf16_round, rel_l2
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def test_bench_graph_rotating_handles_vs_oracle(oracle):
+@pytest.mark.parametrize("pdl_chain", [True, False])
+def test_bench_graph_rotating_handles_vs_oracle(oracle, pdl_chain):
     torch = pytest.importorskip("torch")
     d, F, r, NL, NX, STEPS = 4096, 14336, 512, 8, 16, 48
     g = oracle.generate(42, d, F, r)
@@ -25,6 +26,8 @@ def test_bench_graph_rotating_handles_vs_oracle(oracle):
     pred = cd.Predictor(cd.LowRankPredictor(d, r, F, g["theta_a"], g["theta_b"]), "bf16")
     devs = [cd.GatedMlpLayer(d, F, 0, g["w_up"], g["w_gate"], g["w_down"], device_dtype="bf16").device_layer(pred)
             for _ in range(NL)]
+    for dv in devs:
+        dv.set_engines(pdl_chain=pdl_chain)  # the bench's mode (True) and the library default
     X = np.stack([cd.synth_normals(9000 + i, d) for i in range(NX)])
     Z = np.stack([oracle.lowrank_logits(g["theta_a"], g["theta_b"], x)[1] for x in X])
     tau = float(np.mean([np.quantile(z, 0.9) for z in Z]))

@@ -21,6 +21,8 @@ d, F, r, NL, NX, STEPS = 4096, 14336, 512, 8, 16, 400
 layer, _, pred = cd.synth_workload(42, d, F, r, device_dtype="bf16")
 devs = [layer.device_layer(pred)] + [cd.GatedMlpLayer(d, F, 0, layer.w_up, layer.w_gate, layer.w_down,
                                                       device_dtype="bf16").device_layer(pred) for _ in range(NL - 1)]
+for dv in devs:
+    dv.set_engines(pdl_chain=os.environ.get("AB_COOP") != "1")
 X = np.stack([cd.synth_normals(1000 + i, d) for i in range(NX)])
 mid = {"dc": cd._capi.METHOD_DC, "mc": cd._capi.METHOD_MC, "dense": cd._capi.METHOD_DENSE}[method]
 if method == "dc":

@@ -29,6 +29,8 @@ d, F, r, NL, NX, STEPS = 4096, 14336, 512, 8, 16, 400
 layer, _, pred = cd.synth_workload(42, d, F, r, device_dtype="bf16")
 devs = [layer.device_layer(pred)] + [cd.GatedMlpLayer(d, F, 0, layer.w_up, layer.w_gate, layer.w_down,
                                                       device_dtype="bf16").device_layer(pred) for _ in range(NL - 1)]
+for dv in devs:
+    dv.set_engines(pdl_chain=os.environ.get("AB_COOP") != "1")
 X = np.stack([cd.synth_normals(1000 + i, d) for i in range(NX)])
 z = devs[0].predict_logits(X)
 tau = float(np.mean([np.quantile(z[i], k) for i in range(NX)]))

@@ -5,6 +5,7 @@
 // kernels_fast.cu (UnorderedAccumulate) and kernels_exact.cu (DeterministicOrdered).
 // No CPU compute path exists: every operator runs on the device or fails.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a profiler
 
 #include <algorithm>
 #include <cerrno>
@@ -465,7 +466,14 @@ struct HostIO {
     int64_t* alive_out = nullptr;
 };
 
+// NVTX range for the length of a scope (host-side enqueue of one operator call)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 void host_call(cd_layer* h, Req base, int64_t batch, const HostIO& io) {
+    NvtxRange nv("cd.host_call");
     CallLock lk(h);
     ck(cudaSetDevice(h->device), "cudaSetDevice");
     const int64_t d = h->L.d, F = h->L.F;
@@ -1231,6 +1239,7 @@ int cd_predict_logits(cd_layer* h, int64_t batch, const float* x, float* logits)
 int cd_forward_device(cd_layer* h, int method, int64_t batch, const float* d_x, float tau, int reduction,
                       const uint8_t* d_mask_override, float* d_y, uint8_t* d_mask, float* d_indicator,
                       int32_t* d_alive, void* stream) {
+    NvtxRange nv("cd.forward_device");
     return guarded([&] {
         check_common(h, batch, d_x, d_y);
         check_reduction(reduction);
@@ -1259,6 +1268,7 @@ int cd_forward_device(cd_layer* h, int method, int64_t batch, const float* d_x, 
 int cd_forward_device_normed(cd_layer* h, int method, int64_t batch, const float* d_x, float rms_eps, float tau,
                              int reduction, const uint8_t* d_mask_override, float* d_y, uint8_t* d_mask,
                              float* d_indicator, int32_t* d_alive, void* stream) {
+    NvtxRange nv("cd.forward_device_normed");
     return guarded([&] {
         check_common(h, batch, d_x, d_y);
         check_reduction(reduction);

@@ -37,12 +37,37 @@ def shard_range(d_inter: int, world: int, rank: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < rem else 0)
 
 
+class nvtx_range:
+    """NVTX range around host-side enqueueing (a no-op without CUDA / a profiler attached), so
+    an nsys / ncu timeline shows each layer and each all-reduce."""
+
+    def __init__(self, name: str):
+        self.name = name
+        self.on = False
+
+    def __enter__(self):
+        try:
+            import torch
+            if torch.cuda.is_available():
+                torch.cuda.nvtx.range_push(self.name)
+                self.on = True
+        except Exception:
+            self.on = False
+        return self
+
+    def __exit__(self, *a):
+        if self.on:
+            import torch
+            torch.cuda.nvtx.range_pop()
+
+
 def allreduce_sum_(y, group=None):
     """In-place sum of the ranks' partial outputs (a torch tensor; NCCL over NVLink on the
     device, gloo on CPU).  Enqueued on the caller's current stream context."""
     import torch.distributed as dist
     if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+        with nvtx_range("cd.allreduce"):
+            dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
     return y
 
 
@@ -66,8 +91,9 @@ class TPLayer:
     def forward_local(self, method: int, x_dev, y_dev, tau: float, stream: int, batch: int = 1,
                       alive_out=None) -> None:
         """This rank's partial y over its neuron slice (no communication)."""
-        self.dev.forward_device(method, x_dev, y_dev, tau, Reduction.UnorderedAccumulate, batch,
-                                alive_out=alive_out, stream=stream)
+        with nvtx_range("cd.layer"):
+            self.dev.forward_device(method, x_dev, y_dev, tau, Reduction.UnorderedAccumulate, batch,
+                                    alive_out=alive_out, stream=stream)
 
     def forward(self, method: int, x_dev, y_dev, tau: float, stream: int, batch: int = 1,
                 alive_out=None) -> None:
@@ -146,11 +172,12 @@ class TPStack:
         alive count."""
 
         def run_layer(l, x_in, y_out, normed):
-            self.tps[l].dev.forward_device(
-                self.method, x_in, y_out, self.taus[l], Reduction.UnorderedAccumulate, batch,
-                mask_out=None if masks_out is None else masks_out[l],
-                alive_out=None if alive_out is None else alive_out[l], stream=stream,
-                rms_eps=self.eps if normed else None)
+            with nvtx_range(f"cd.layer{l}"):
+                self.tps[l].dev.forward_device(
+                    self.method, x_in, y_out, self.taus[l], Reduction.UnorderedAccumulate, batch,
+                    mask_out=None if masks_out is None else masks_out[l],
+                    alive_out=None if alive_out is None else alive_out[l], stream=stream,
+                    rms_eps=self.eps if normed else None)
 
         stack_step(len(self.tps), x_dev, ys_dev, run_layer,
                    (lambda y: allreduce_sum_(y, self.group)) if comm else (lambda y: None))

@@ -817,7 +817,7 @@ cd_layer* create_impl(int device, int64_t d, int64_t F_total, int64_t rb, int64_
         S.done = cv.take<int>(1);
         S.alive = cv.take<int>(kMaxBatch);
         S.ctl = cv.take<unsigned>(128);
-        S.t_list = cv.take<unsigned long long>(Fz);
+        S.t_list = cv.take<unsigned long long>(Fz + cdk::kMaxCtas);  // per-CTA regions of ceil(F/G)
         S.t_aux = cv.take<unsigned long long>(Fz);
         S.t_count = cv.take<unsigned long long>(cdk::kMaxCtas);
         S.t_alive = cv.take<unsigned long long>(cdk::kMaxCtas * kMaxBatchFast);

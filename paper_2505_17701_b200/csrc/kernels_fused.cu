@@ -439,9 +439,11 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             for (int j = 0; j < VPT; ++j) {
                 const int vec = ct + j * nc;
                 if (vec < nvec) {
-                    float4* dst = reinterpret_cast<float4*>(xs + (int64_t)vec * kVec);
-                    dst[0] = make_float4(xr[0][j][0], xr[0][j][1], xr[0][j][2], xr[0][j][3]);
-                    dst[1] = make_float4(xr[0][j][4], xr[0][j][5], xr[0][j][6], xr[0][j][7]);
+                    // two planes (elements 0-3 / 4-7 of every 8-vector): a dot warp's lanes then
+                    // read consecutive 16-byte words (no 2-way bank conflict)
+                    float4* lo = reinterpret_cast<float4*>(xs);
+                    lo[vec] = make_float4(xr[0][j][0], xr[0][j][1], xr[0][j][2], xr[0][j][3]);
+                    lo[nvec + vec] = make_float4(xr[0][j][4], xr[0][j][5], xr[0][j][6], xr[0][j][7]);
                 }
             }
         }
@@ -545,7 +547,10 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int e = e0 + k * nc;
-                const int b = e / (int)L.ldr, q = e % (int)L.ldr;
+                int b = 0;
+#pragma unroll
+                for (int bb = 1; bb < NB; ++bb) b += e >= bb * (int)L.ldr;
+                const int q = e - b * (int)L.ldr;
                 w[k] = (e < NB * (int)L.ldr && b < nb && q < L.r) ? ld_relaxed_u64(t_lat + e) : tagged(tag, 0u);
             }
 #pragma unroll
@@ -553,7 +558,14 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 const int e = e0 + k * nc;
                 if (e >= NB * (int)L.ldr) continue;
                 if (static_cast<uint32_t>(w[k] >> 32) != tag) w[k] = tagged(tag, await_relaxed(t_lat + e, tag));
-                latbuf[e] = __uint_as_float(static_cast<uint32_t>(w[k]));
+                // two planes per sample (elements 0-3 / 4-7 of every 8-vector): the stage-2 reads
+                // of a warp are then consecutive 16-byte words (no 2-way bank conflict)
+                int b = 0;
+#pragma unroll
+                for (int bb = 1; bb < NB; ++bb) b += e >= bb * (int)L.ldr;  // no runtime division
+                const int q = e - b * (int)L.ldr;
+                latbuf[b * L.ldr + ((q & 4) ? L.ldr / 2 : 0) + (q >> 3) * 4 + (q & 3)] =
+                    __uint_as_float(static_cast<uint32_t>(w[k]));
             }
         }
         named_bar_sync(kBarC, nc);
@@ -567,9 +579,8 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 for (int b = 0; b < NB; ++b) {
                     float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
                     if (vec < nvr) {
-                        const float4* src = reinterpret_cast<const float4*>(latbuf + b * L.ldr + vec * kVec);
-                        lo = src[0];
-                        hi = src[1];
+                        lo = reinterpret_cast<const float4*>(latbuf + b * L.ldr)[vec];
+                        hi = reinterpret_cast<const float4*>(latbuf + b * L.ldr + L.ldr / 2)[vec];
                     }
                     lat[b][v][0] = lo.x; lat[b][v][1] = lo.y; lat[b][v][2] = lo.z; lat[b][v][3] = lo.w;
                     lat[b][v][4] = hi.x; lat[b][v][5] = hi.y; lat[b][v][6] = hi.z; lat[b][v][7] = hi.w;
@@ -639,9 +650,8 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             for (int b = 0; b < NB; ++b) {
                 float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
                 if (vec < nvr) {
-                    const float4* src = reinterpret_cast<const float4*>(latbuf + b * L.ldr + vec * kVec);
-                    lo = src[0];
-                    hi = src[1];
+                    lo = reinterpret_cast<const float4*>(latbuf + b * L.ldr)[vec];
+                    hi = reinterpret_cast<const float4*>(latbuf + b * L.ldr + L.ldr / 2)[vec];
                 }
                 lat[b][v][0] = lo.x; lat[b][v][1] = lo.y; lat[b][v][2] = lo.z; lat[b][v][3] = lo.w;
                 lat[b][v][4] = hi.x; lat[b][v][5] = hi.y; lat[b][v][6] = hi.z; lat[b][v][7] = hi.w;
@@ -846,12 +856,14 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             for (int j = 0; j < VPT; ++j) {
                 const int vec = ct + j * nc;
 #pragma unroll
-                for (int b = 0; b < NB; ++b)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int64_t col = (int64_t)vec * kVec + k;
-                        if (b < nb && vec < nvec && col < L.d) ys[b * L.d + col] = yr[b][j][k];
-                    }
+                for (int b = 0; b < NB; ++b) {
+                    // d % 4 == 0 (launch requirement): whole float4s (scalar stores conflict 8-way)
+                    const int64_t col = (int64_t)vec * kVec;
+                    if (b >= nb || vec >= nvec) continue;
+                    float4* dst = reinterpret_cast<float4*>(ys + b * L.d + col);
+                    if (col < L.d) dst[0] = make_float4(yr[b][j][0], yr[b][j][1], yr[b][j][2], yr[b][j][3]);
+                    if (col + 4 < L.d) dst[1] = make_float4(yr[b][j][4], yr[b][j][5], yr[b][j][6], yr[b][j][7]);
+                }
             }
             fence_proxy_async_smem();
             named_bar_sync(kBarC, nc);
@@ -865,17 +877,22 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         const int64_t row_bytes = L.ld * (int64_t)sizeof(W);
         if (warp < n_dot) {
             // dot warp: records warp, warp + n_dot, ... of the stage sequence
+            int sq = warp;  // e % nstages and its use parity, advanced without a division
+            uint32_t upar = 0;
             for (int e = warp;; e += n_dot) {
-                const int sq = e % nstages;
+                if (e != warp) {
+                    sq += n_dot;
+                    if (sq >= nstages) { sq -= nstages; upar ^= 1u; }
+                }
                 // the stage's previous use (e - nstages) may still be loading: its incomplete
                 // phase has the other parity, so the wait can return early -- retry until the
                 // stage holds record e
                 // (meta.seq == e implies the previous use completed, so the second wait is exact)
                 for (;;) {
-                    mbar_wait(&full[sq], static_cast<uint32_t>(e / nstages) & 1u);
+                    mbar_wait(&full[sq], upar);
                     if (*reinterpret_cast<volatile int32_t*>(&meta[sq].seq) == e) break;
                 }
-                mbar_wait(&full[sq], static_cast<uint32_t>(e / nstages) & 1u);
+                mbar_wait(&full[sq], upar);
                 if (meta[sq].idx < 0) {
                     // this warp's sentinel: forward it (the down warps stop at the first one)
                     if (lane == 0) mbar_arrive(&sready[sq]);
@@ -898,8 +915,8 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                     float wu[8], wg[8];
                     Vec8<W>::load(rup + v * kVec, wu);
                     Vec8<W>::load(rgate + v * kVec, wg);
-                    const float4 xa = reinterpret_cast<const float4*>(xs)[2 * v];
-                    const float4 xb = reinterpret_cast<const float4*>(xs)[2 * v + 1];
+                    const float4 xa = reinterpret_cast<const float4*>(xs)[v];
+                    const float4 xb = reinterpret_cast<const float4*>(xs)[nvec + v];
                     const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
                     for (int k = 0; k < 8; k += 2) {
@@ -928,9 +945,11 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
 #pragma unroll
                 for (int k = 0; k < 8; ++k) yd[j][k] = 0.0f;
             int n_rec = 0;
-            for (int e = 0;; ++e) {
-                const int sq = e % nstages;
-                mbar_wait(&sready[sq], static_cast<uint32_t>(e / nstages) & 1u);
+            int sq = -1;
+            uint32_t upar = 0;
+            for (;;) {
+                if (++sq == nstages) { sq = 0; upar ^= 1u; }
+                mbar_wait(&sready[sq], upar);
                 if (meta[sq].idx < 0) break;
                 const float sv = svs[sq];
                 const W* rdown = reinterpret_cast<const W*>(ring + sq * stage_bytes + 2 * row_bytes);
@@ -957,12 +976,12 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
 #pragma unroll
                 for (int j = 0; j < kVPD; ++j) {
                     const int vec = td + j * nd;
-                    if (vec < nvec)
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const int64_t col = (int64_t)vec * kVec + k;
-                            if (col < L.d) ys[col] = yd[j][k];
-                        }
+                    if (vec < nvec) {
+                        // d % 4 == 0 (launch requirement): whole float4s, 8 lanes per 128 bytes
+                        float4* dst = reinterpret_cast<float4*>(ys + (int64_t)vec * kVec);
+                        if ((int64_t)vec * kVec < L.d) dst[0] = make_float4(yd[j][0], yd[j][1], yd[j][2], yd[j][3]);
+                        if ((int64_t)vec * kVec + 4 < L.d) dst[1] = make_float4(yd[j][4], yd[j][5], yd[j][6], yd[j][7]);
+                    }
                 }
                 fence_proxy_async_smem();
                 named_bar_sync(kBarD, nd);
@@ -1057,7 +1076,6 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     const bool split3 = regb && nbk == 1;
     if (split3) nwc64 = std::max<int64_t>(nwc64, 10);
     const int nwc = static_cast<int>(nwc64);
-    const int n_dot = split3 ? nwc - 8 : 0;
     if (split3 && (nvec + 8 * kWarp - 1) / (8 * kWarp) > 4) return cudaErrorInvalidValue;
     if (nwc * kWarp > kMaxConsumers) return cudaErrorInvalidValue;
     const int threads = (nwc + 1) * kWarp;
@@ -1070,6 +1088,10 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
     const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
     if (nstages < 2) return cudaErrorInvalidValue;
+    // dot warps run at most nstages - 1 records ahead of the stage sequence (their parity waits
+    // are sequence-checked against one previous use of a stage)
+    const int n_dot = split3 ? std::min(nwc - 8, nstages - 1) : 0;
+    if (split3 && n_dot < 1) return cudaErrorInvalidValue;
     static const bool bsmem_env = dev_knob("CD_DC_BSMEM", 1) != 0;
     const int b_smem = regb && bsmem_env && (int64_t)rpc * brow_bytes + aux_bytes <= stage_bytes * nstages ? 1 : 0;
     if (regb ? rpc > nwc * 8 : (int64_t)rpc * brow_bytes + aux_bytes > stage_bytes * nstages)

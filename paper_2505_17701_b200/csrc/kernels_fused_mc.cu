@@ -406,12 +406,13 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
             float* ys = reinterpret_cast<float*>(ring);
 #pragma unroll
             for (int j = 0; j < VPT; ++j) {
+                // d % 4 == 0 (launch requirement): whole float4s (scalar stores conflict 8-way)
                 const int vec = ct + j * nc;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int64_t col = (int64_t)vec * kVec + k;
-                    if (vec < nvec && col < L.d) ys[col] = yr[j][k];
-                }
+                const int64_t col = (int64_t)vec * kVec;
+                if (vec >= nvec) continue;
+                float4* dst = reinterpret_cast<float4*>(ys + col);
+                if (col < L.d) dst[0] = make_float4(yr[j][0], yr[j][1], yr[j][2], yr[j][3]);
+                if (col + 4 < L.d) dst[1] = make_float4(yr[j][4], yr[j][5], yr[j][6], yr[j][7]);
             }
             fence_proxy_async_smem();
             named_bar_sync(kBarC, nc);

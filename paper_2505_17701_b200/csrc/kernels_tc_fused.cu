@@ -359,6 +359,58 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
         }
         // ---- phase A: gate/up tiles (contributors park partials, finishers apply the masks)
         for (int si = 0; seg_at(c, si, UA, G, nkbA, sg); ++si) {
+            // Finisher of a split tile: its contributors parked their partials long ago (their
+            // first segments), so pull them into free TMEM columns now, while this segment's MMAs
+            // still run -- the epilogue then reads them from TMEM instead of walking a chain of
+            // global round trips after the last k-block (the phase A -> B gap).
+            int c_last = c;
+            bool staged = false;
+            uint32_t pb = 0;
+            bool pz = false;  // the finisher holds Z: the contributors hold only Z (one column block)
+            if (sg.kb0 == 0) {
+                const int64_t tb = static_cast<int64_t>(sg.tile) * nkbA;
+                while (c_last + 1 < G && range_lo(c_last + 1, UA, G) < tb + nkbA) ++c_last;
+                if (c_last > c) {
+                    if (et == 0) {
+                        for (int cc = c + 1; cc <= c_last; ++cc) {
+                            if (range_lo(cc, UA, G) == range_lo(cc + 1, UA, G)) continue;  // empty range
+                            unsigned* f = a.flags + cc;
+                            while (ld_acquire_u32(f) == 0u) {
+                            }
+                            *f = 0u;  // consumed: ready for the next launch
+                        }
+                    }
+                    __threadfence();
+                    named_bar_sync(1, kEpiThreads);
+                    pz = kZ && sg.kb1 > a.kb_x;
+                    pb = static_cast<uint32_t>((pz ? 3 : 2) * N);
+                    staged = pb + static_cast<uint32_t>(kParts * nbt) <= static_cast<uint32_t>(a.tmem_cols);
+                    if (staged) {
+                        const int64_t slot_floats = static_cast<int64_t>(kParts) * nbt * kBM;
+                        const int sb0 = half * hb;
+#pragma unroll
+                        for (int q = 0; q < kParts; ++q) {
+                            if (pz && q != 2) continue;
+                            for (int cb = sb0; cb < sb0 + hb; cb += kC) {
+                                float v[kC];
+#pragma unroll
+                                for (int j = 0; j < kC; ++j) v[j] = 0.0f;
+                                for (int cc = c + 1; cc <= c_last; ++cc) {
+                                    const int64_t q0 = range_lo(cc, UA, G) - tb, q1 = range_lo(cc + 1, UA, G) - tb;
+                                    if (q0 == q1 || (q == 2 ? !(q1 > a.kb_x) : !(q0 < a.kb_x))) continue;
+                                    const float4* p4 = reinterpret_cast<const float4*>(
+                                        a.ws + cc * slot_floats + (static_cast<int64_t>(q) * kBM + m) * nbt + cb);
+                                    const float4 x0 = __ldcg(p4), x1 = __ldcg(p4 + 1);
+                                    v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
+                                    v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
+                                }
+                                tmem_st8(trow + pb + (pz ? 0u : static_cast<uint32_t>(q * nbt)) + cb, v);
+                            }
+                        }
+                        tmem_wait_st();
+                    }
+                }
+            }
             wait_seg();
             if (et == 0 && sg.kb0 == 0) fstamp(a, 7);
             const bool has_z = kZ && sg.kb1 > a.kb_x;
@@ -388,22 +440,8 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
             }
             const int tile = sg.tile;
             const int64_t tile_base = static_cast<int64_t>(tile) * nkbA;
-            // contributors: the following CTAs whose (non-empty) ranges start inside this tile
-            int c_last = c;
-            while (c_last + 1 < G && range_lo(c_last + 1, UA, G) < tile_base + nkbA) ++c_last;
-            if (c_last > c) {
-                if (et == 0) {
-                    for (int cc = c + 1; cc <= c_last; ++cc) {
-                        if (range_lo(cc, UA, G) == range_lo(cc + 1, UA, G)) continue;  // empty range
-                        unsigned* f = a.flags + cc;
-                        while (ld_acquire_u32(f) == 0u) {
-                        }
-                        *f = 0u;
-                    }
-                }
-                __threadfence();
-                named_bar_sync(1, kEpiThreads);
-            }
+            // contributors (the following CTAs whose non-empty ranges start inside this tile):
+            // their flags were consumed above, their partials staged in TMEM when they fit
             if (et == 0) fstamp(a, 6);
             const int i = (tile / a.n_tiles) * kBM + m;
             const bool valid = i < a.F;
@@ -434,7 +472,7 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
                     }
                 }
             };
-            if (c_last > c) load_partials(sb0, pre);
+            if (c_last > c && !staged) load_partials(sb0, pre);
             for (int cb = sb0; cb < sb0 + hb; cb += kC, s_hi += kC * ld_s) {
                 float acc[kParts][2][kC];
 #pragma unroll
@@ -450,7 +488,21 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
                         }
                     }
                 }
-                if (c_last > c) {
+                if (staged) {
+                    float pv[kParts][kC];
+#pragma unroll
+                    for (int q = 0; q < kParts; ++q) {
+                        if (pz && q != 2) continue;
+                        tmem_ld8(trow + pb + (pz ? 0u : static_cast<uint32_t>(q * nbt)) + cb, pv[q]);
+                    }
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int q = 0; q < kParts; ++q) {
+                        if (pz && q != 2) continue;
+#pragma unroll
+                        for (int j = 0; j < kC; ++j) acc[q][0][j] += pv[q][j];
+                    }
+                } else if (c_last > c) {
                     float4 cur[kParts][2];
 #pragma unroll
                     for (int q = 0; q < kParts; ++q) cur[q][0] = pre[q][0], cur[q][1] = pre[q][1];
@@ -677,8 +729,9 @@ cudaError_t launch_batched_fused(const LayerDev& L, const Plan& p, void* ws_base
     a.tl = tl_env;
     static const int pf_env = dev_knob("CD_TC_PB_PF", 0);
     a.pb_pf = pf_env;
-    const int cols_used = dc_pred ? 3 * p.N : 2 * p.N;
-    a.tmem_cols = cols_used <= 64 ? 64 : cols_used <= 128 ? 128 : cols_used <= 256 ? 256 : 512;
+    // all 512 columns (one CTA per SM): the accumulators plus room to stage a tile's contributor
+    // partials next to them
+    a.tmem_cols = 512;
     const int stage_bytes = 2 * kABytes + p.N * kBK * 2;
     const size_t fixed = 1024 + 256;
     a.stages = static_cast<int>(std::min<size_t>(16, (kMaxDynSmem - fixed) / stage_bytes));

@@ -158,6 +158,8 @@ cudaError_t launch_count_nonfinite(const float* v, int64_t n, int* out, cudaStre
 
 // One-thread kernel that occupies the stream for `ns` nanoseconds (timing helper).
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t s);
+cudaError_t launch_copy_out_signal(float* hy, const float* dy, int64_t ny, int* ha, const int* da, int na,
+                                   unsigned long long* done, cudaStream_t s, bool pdl);
 
 // Development build only (-DCD_TIMELINE): copy the per-CTA phase stamps to the host.
 cudaError_t read_timeline(unsigned long long* out, int64_t n);

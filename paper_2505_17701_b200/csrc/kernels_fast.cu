@@ -747,6 +747,9 @@ cudaError_t read_timeline(unsigned long long*, int64_t) { return cudaErrorNotSup
 // Small host<->device staging copies as a kernel over mapped pinned memory: no copy-engine
 // round trip (a 16 KB DMA costs ~10 us of latency in a synchronous call; this ~1-2 us).
 __global__ void k_copy_bytes(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t n) {
+    // a PDL-launched successor (the step kernel) may start its weight prologue now; it waits on
+    // griddepcontrol.wait for this copy before touching the input
+    pdl_launch_dependents();
     const size_t i0 = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x * 16;
     const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
@@ -809,6 +812,39 @@ cudaError_t launch_copy(void* dst, const void* src, size_t bytes, cudaStream_t s
     k_copy_bytes<<<static_cast<unsigned>(blocks < 64 ? blocks : 64), 256, 0, s>>>(
         static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes);
     return cudaGetLastError();
+}
+
+// The host-buffer call's outputs to mapped pinned memory in ONE kernel (y, then the alive
+// counts), then a completion word the host polls instead of a stream synchronisation: one CTA,
+// __threadfence_system() orders the payload before the word (incremented per call: a captured
+// graph replays the same kernel).
+__global__ void k_copy_out_signal(float* __restrict__ hy, const float* __restrict__ dy, int64_t ny,
+                                  int* __restrict__ ha, const int* __restrict__ da, int na,
+                                  unsigned long long* done) {
+    pdl_wait();  // launched PDL behind the step kernel: resident early, waits for its y here
+    if ((ny & 3) == 0 && ((reinterpret_cast<uintptr_t>(hy) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0) {
+        for (int64_t i = threadIdx.x; i < ny / 4; i += blockDim.x)
+            reinterpret_cast<float4*>(hy)[i] = reinterpret_cast<const float4*>(dy)[i];
+    } else {
+        for (int64_t i = threadIdx.x; i < ny; i += blockDim.x) hy[i] = dy[i];
+    }
+    for (int i = threadIdx.x; i < na; i += blockDim.x) ha[i] = da[i];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned long long* w = done;
+        *w = *w + 1ull;
+        __threadfence_system();
+    }
+}
+
+cudaError_t launch_copy_out_signal(float* hy, const float* dy, int64_t ny, int* ha, const int* da, int na,
+                                   unsigned long long* done, cudaStream_t s, bool pdl) {
+    // 128 threads: small enough to be co-resident with the step kernel's CTA on an SM
+    LaunchCfg c;
+    c.stream = s;
+    c.pdl = pdl;
+    return launch_ex(k_copy_out_signal, dim3(1), dim3(128), 0, c, pdl, hy, dy, ny, ha, da, na, done);
 }
 
 cudaError_t launch_spin(unsigned long long ns, cudaStream_t s) {

@@ -39,6 +39,10 @@ def timeit(name, fn):
 
 timeit("(a) cd_pipeline_dc host call", lambda: check(L.cd_pipeline_dc(dev.raw, 1, ptr(x), tau, None, 1, ptr(yh), None,
                                                                      ptr(ah), None)))
+dev.set_engines(pdl_chain=True)
+timeit("(a2) cd_pipeline_dc host call, PDL chain", lambda: check(L.cd_pipeline_dc(dev.raw, 1, ptr(x), tau, None, 1,
+                                                                              ptr(yh), None, ptr(ah), None)))
+dev.set_engines()
 xd = torch.from_numpy(x).cuda()
 yd = torch.empty(D, device="cuda")
 s = torch.cuda.Stream()

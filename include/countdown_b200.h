@@ -120,7 +120,7 @@ CD_API int cd_layer_last_launches(const cd_layer* h, int* launches);
 
 /* Engine that ran the most recent forward call: CD_PATH_EXACT (ordered folds, CUDA cores),
  * CD_PATH_FAST (fused sparse kernels, CUDA cores, batch chunks of 4) or CD_PATH_TENSOR
- * (bf16 layer at batch >= 8: masked row-union GEMM on the tcgen05 tensor cores). */
+ * (bf16 layer at batch >= 8, M-CountDown / CATS from batch 3: masked row-union GEMM on the tcgen05 tensor cores). */
 #define CD_PATH_EXACT 0
 #define CD_PATH_FAST 1
 #define CD_PATH_TENSOR 2

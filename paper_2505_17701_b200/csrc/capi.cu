@@ -264,6 +264,11 @@ struct Req {
 };
 
 constexpr int kTcMinBatch = 8;  // batches from here on run on the tensor cores (bf16 layers)
+// M-CountDown / CATS at batch 2-7: their CUDA-core path is two kernels (a dense W_up / W_gate
+// GEMV, then the union records), register-bound at 2-4 samples (Gemma B=4: 116 us, 0.23 of
+// HBM); the row-union GEMM streams all rows but at ~0.6 of HBM (72 us) -- it wins from batch 3
+// (measured: B=2 59.7 vs 71.7 us, B=3 105.5 vs 71.6, B=4 122.1 vs 71.5)
+constexpr int kTcMinBatchMC = 3;
 
 // The tensor-core path (kernels_tc.cu) covers bf16 layers at batch >= 8 for the calls that
 // threshold their own masks (pipelines, dense).  Caller-supplied masks -- exec_dc / exec_mc /
@@ -272,7 +277,8 @@ constexpr int kTcMinBatch = 8;  // batches from here on run on the tensor cores 
 // poison them with NaN, test_blocked_exec.cpp:101-116), while the row-union GEMM reads every
 // row and 0 x NaN would reach y.
 bool tc_eligible(const cd_layer* h, const Req& r) {
-    if (!h->use_tc || h->L.dtype != CD_DTYPE_BF16 || !h->L.w_up || r.nb < kTcMinBatch || r.marks) return false;
+    const int min_nb = (r.method == cdk::kMC || r.method == cdk::kCATS) ? kTcMinBatchMC : kTcMinBatch;
+    if (!h->use_tc || h->L.dtype != CD_DTYPE_BF16 || !h->L.w_up || r.nb < min_nb || r.marks) return false;
     if (!h->weights_finite) return false;
     if (r.reduction != CD_REDUCTION_UNORDERED) return false;
     if (r.with_masks || r.ovr) return false;

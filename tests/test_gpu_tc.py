@@ -70,7 +70,7 @@ def test_tc_dc_pipeline(oracle, shape, B):
 
 
 @pytest.mark.parametrize("act", [0, 1])
-@pytest.mark.parametrize("B", [8, 33, 64])
+@pytest.mark.parametrize("B", [3, 5, 8, 33, 64])  # M-CountDown takes the tensor cores from batch 3
 @pytest.mark.parametrize("shape", TC_SHAPES[1:])
 def test_tc_mc_pipeline(oracle, shape, B, act):
     seed, d, F, r = shape
@@ -86,7 +86,7 @@ def test_tc_mc_pipeline(oracle, shape, B, act):
         assert rel_l2(res.y[b], oracle.forward_sparse(g, X[b], res.mask[b].alive, act=act)) <= 1e-4
 
 
-@pytest.mark.parametrize("B", [8, 40])
+@pytest.mark.parametrize("B", [3, 8, 40])
 def test_tc_cats_pipeline(oracle, B):
     seed, d, F, r = 202, 200, 300, 40
     g, layer, _ = make(oracle, seed, d, F, r, 1)

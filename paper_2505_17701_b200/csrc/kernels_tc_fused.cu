@@ -391,20 +391,26 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
 #pragma unroll
                         for (int q = 0; q < kParts; ++q) {
                             if (pz && q != 2) continue;
-                            for (int cb = sb0; cb < sb0 + hb; cb += kC) {
-                                float v[kC];
+                            // the whole half (<= 32 samples) of this row per contributor: all
+                            // loads in flight at once (coalesced: [part][sample][row] slots)
+                            float v[32];
 #pragma unroll
-                                for (int j = 0; j < kC; ++j) v[j] = 0.0f;
-                                for (int cc = c + 1; cc <= c_last; ++cc) {
-                                    const int64_t q0 = range_lo(cc, UA, G) - tb, q1 = range_lo(cc + 1, UA, G) - tb;
-                                    if (q0 == q1 || (q == 2 ? !(q1 > a.kb_x) : !(q0 < a.kb_x))) continue;
-                                    const float4* p4 = reinterpret_cast<const float4*>(
-                                        a.ws + cc * slot_floats + (static_cast<int64_t>(q) * kBM + m) * nbt + cb);
-                                    const float4 x0 = __ldcg(p4), x1 = __ldcg(p4 + 1);
-                                    v[0] += x0.x; v[1] += x0.y; v[2] += x0.z; v[3] += x0.w;
-                                    v[4] += x1.x; v[5] += x1.y; v[6] += x1.z; v[7] += x1.w;
-                                }
-                                tmem_st8(trow + pb + (pz ? 0u : static_cast<uint32_t>(q * nbt)) + cb, v);
+                            for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+                            for (int cc = c + 1; cc <= c_last; ++cc) {
+                                const int64_t q0 = range_lo(cc, UA, G) - tb, q1 = range_lo(cc + 1, UA, G) - tb;
+                                if (q0 == q1 || (q == 2 ? !(q1 > a.kb_x) : !(q0 < a.kb_x))) continue;
+                                const float* src = a.ws + cc * slot_floats + (static_cast<int64_t>(q) * nbt + sb0) * kBM + m;
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    if (j < hb) v[j] += __ldcg(src + static_cast<int64_t>(j) * kBM);
+                            }
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                if (k * kC >= hb) break;
+                                float v8[kC];
+#pragma unroll
+                                for (int j = 0; j < kC; ++j) v8[j] = v[k * kC + j];
+                                tmem_st8(trow + pb + (pz ? 0u : static_cast<uint32_t>(q * nbt)) + sb0 + k * kC, v8);
                             }
                         }
                         tmem_wait_st();
@@ -425,11 +431,10 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
                         tmem_ld16(trow + q * N + c0, v);
                         tmem_ld16(trow + q * N + nbt + c0, w);
                         tmem_wait_ld();
-                        float4* dst = reinterpret_cast<float4*>(slot + (static_cast<int64_t>(q) * kBM + m) * nbt + c0);
+                        // slot layout [part][sample][row]: a warp's stores are 128 consecutive bytes
+                        float* dst = slot + (static_cast<int64_t>(q) * nbt + c0) * kBM + m;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            dst[j] = make_float4(v[4 * j] + w[4 * j], v[4 * j + 1] + w[4 * j + 1],
-                                                 v[4 * j + 2] + w[4 * j + 2], v[4 * j + 3] + w[4 * j + 3]);
+                        for (int j = 0; j < 16; ++j) dst[static_cast<int64_t>(j) * kBM] = v[j] + w[j];
                     }
                 }
                 done_seg();
@@ -461,14 +466,15 @@ k_tc_fused(const __grid_constant__ CUtensorMap m_up, const __grid_constant__ CUt
                     const int64_t q0 = range_lo(cc, UA, G) - tile_base;
                     const int64_t q1 = range_lo(cc + 1, UA, G) - tile_base;
                     if (q0 == q1) continue;  // empty range
-                    const float* gp = a.ws + cc * slot_floats + static_cast<int64_t>(m) * nbt + cb;
+                    const float* gp = a.ws + cc * slot_floats + static_cast<int64_t>(cb) * kBM + m;
 #pragma unroll
                     for (int q = 0; q < kParts; ++q) {
                         if (q == 2 ? !(q1 > a.kb_x) : !(q0 < a.kb_x)) continue;
-                        const float4* p4 = reinterpret_cast<const float4*>(gp + static_cast<int64_t>(q) * kBM * nbt);
-                        const float4 x0 = __ldcg(p4), x1 = __ldcg(p4 + 1);
-                        d[q][0].x += x0.x; d[q][0].y += x0.y; d[q][0].z += x0.z; d[q][0].w += x0.w;
-                        d[q][1].x += x1.x; d[q][1].y += x1.y; d[q][1].z += x1.z; d[q][1].w += x1.w;
+                        const float* p = gp + static_cast<int64_t>(q) * nbt * kBM;  // [part][sample][row]
+                        d[q][0].x += __ldcg(p); d[q][0].y += __ldcg(p + kBM);
+                        d[q][0].z += __ldcg(p + 2 * kBM); d[q][0].w += __ldcg(p + 3 * kBM);
+                        d[q][1].x += __ldcg(p + 4 * kBM); d[q][1].y += __ldcg(p + 5 * kBM);
+                        d[q][1].z += __ldcg(p + 6 * kBM); d[q][1].w += __ldcg(p + 7 * kBM);
                     }
                 }
             };

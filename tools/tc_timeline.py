@@ -40,3 +40,14 @@ for method in (_capi.METHOD_MC, _capi.METHOD_DC):
             continue
         print(f"  {name:8s} min {np.nanmin(col):7.2f}  med {np.nanmedian(col):7.2f}  max {np.nanmax(col):7.2f}")
 
+    # the CTAs whose phase-A epilogue ends last (they gate "s complete")
+    order = np.argsort(-np.nan_to_num(rel[:, 4]))
+    F_ = F
+    nkbA = (D + 63) // 64 + ((R + 63) // 64 if method == _capi.METHOD_DC else 0)
+    tiles = (F_ + 127) // 128
+    U = tiles * nkbA
+    print("  latest epiA_end: cta | range units [lo, hi) tiles | mmaA_end fin_start epiA_end")
+    for c in order[:6]:
+        lo, hi = c * U // n, (c + 1) * U // n
+        print(f"   {c:4d} | [{lo}, {hi}) tiles {lo // nkbA}..{(hi - 1) // nkbA} | "
+              f"{rel[c, 1]:6.2f} {rel[c, 7]:6.2f} {rel[c, 4]:6.2f}")

@@ -39,6 +39,7 @@ def timeit(name, fn):
 
 timeit("(a) cd_pipeline_dc host call", lambda: check(L.cd_pipeline_dc(dev.raw, 1, ptr(x), tau, None, 1, ptr(yh), None,
                                                                      ptr(ah), None)))
+print("host call launches:", dev.last_launches(), "path:", dev.last_path(), flush=True)
 dev.set_engines(pdl_chain=True)
 timeit("(a2) cd_pipeline_dc host call, PDL chain", lambda: check(L.cd_pipeline_dc(dev.raw, 1, ptr(x), tau, None, 1,
                                                                               ptr(yh), None, ptr(ah), None)))

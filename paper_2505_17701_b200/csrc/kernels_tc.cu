@@ -640,6 +640,11 @@ __global__ void k_tc_zero_tiles(float* __restrict__ y, int nb, int d, int n_jt, 
 }
 
 // ---------------------------------------------------------------- small element-wise kernels
+__global__ void k_tc_fill_int(int* __restrict__ p, int64_t n, int v) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
 __device__ __forceinline__ void split_store4(__nv_bfloat16* hi, __nv_bfloat16* lo, float4 v) {
     const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
     const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
@@ -684,8 +689,9 @@ Plan plan_for(int64_t nb, int method) {
     Plan p;
     // Decode: pairs of bf16 (hi, lo) per activation, up to 64 samples per n-tile (UMMA N = 128).
     // Large dense batches (prefill): single bf16 activations, 256 tokens per n-tile (U and G fill
-    // the 512 TMEM columns; N = 128 with double-buffered accumulators measured 1.5x slower: the
-    // two MMAs per k-step then read 2 x 4 KB of B per 64 cycles, past the shared-memory port).
+    // the 512 TMEM columns; N = 128 with double-buffered accumulators measured 1.27x slower,
+    // 871 vs 685 us at 2048 tokens: the two MMAs per k-step then read 2 x 4 KB of B per 64
+    // cycles, past the shared-memory port).
     p.split = !(method == kDense && nb > 256);
     if (p.split) {
         p.nbt = static_cast<int>(std::min<int64_t>(64, round_up64(nb, 16)));  // epilogue chunks of 16
@@ -739,7 +745,12 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     k_tc_pack_x<<<dim3(static_cast<unsigned>((L.d + 1023) / 1024), static_cast<unsigned>(nb)), 256, 0, c.stream>>>(
         x, L.d, L.ld, 0, p.nbt, xb);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (alive_out && (e = cudaMemsetAsync(alive_out, 0, sizeof(int) * nb, c.stream)) != cudaSuccess) return e;
+    // dense: every neuron is alive for every token -- the count is F, set here instead of the
+    // epilogue's per-token ballots and atomics (7% of the gate/up kernel's stall samples)
+    if (alive_out) {
+        k_tc_fill_int<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, c.stream>>>(alive_out, nb, static_cast<int>(L.F));
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
 
     CUtensorMap m_up, m_gate, m_x;
     if (!make_map(&m_up, L.w_up, L.F, L.d, L.rs, kBM) || !make_map(&m_gate, L.w_gate, L.F, L.d, L.rs, kBM) ||
@@ -758,9 +769,11 @@ cudaError_t launch_batched(const LayerDev& L, const Plan& p, void* ws, unsigned*
     a.ld_s = ld_s;
     a.mask_out = mask_out;
     a.ind_out = ind_out;
-    a.alive_out = alive_out;
-    a.tmem_cols = 2 * p.N <= 256 ? 256 : 512;
-    if (2 * p.N > 512) return cudaErrorInvalidValue;
+    a.alive_out = nullptr;  // dense: filled above
+    a.buf_cols = 2 * p.N;
+    a.nbuf = 4 * p.N <= 512 ? 2 : 1;  // U and G double-buffered when they fit twice
+    a.tmem_cols = a.nbuf * a.buf_cols <= 256 ? 256 : 512;
+    if (a.nbuf * a.buf_cols > 512) return cudaErrorInvalidValue;
     a.n_tiles = p.n_tiles;
     a.tiles = static_cast<int>((L.F + kBM - 1) / kBM) * p.n_tiles;
     a.tl = nullptr;

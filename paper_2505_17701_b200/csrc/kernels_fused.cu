@@ -369,22 +369,28 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         // with thread 0's launch-tag / queue-word reads below.  Plain vector loads, not the TMA
         // engine: a bulk copy of x would queue behind this CTA's predictor prefetch.
         float xr[NB][VPT][8];
+        auto load_x = [&]() {
 #pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            const int vec = ct + j * nc;
+            for (int j = 0; j < VPT; ++j) {
+                const int vec = ct + j * nc;
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
-                const int64_t col = (int64_t)vec * kVec;
-                if (vec < nvec && b < nb) {
-                    const float4* src = reinterpret_cast<const float4*>(x + b * L.d + col);
-                    if (col < L.d) lo = __ldcg(src);
-                    if (col + 4 < L.d) hi = __ldcg(src + 1);
+                for (int b = 0; b < NB; ++b) {
+                    float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+                    const int64_t col = (int64_t)vec * kVec;
+                    if (vec < nvec && b < nb) {
+                        const float4* src = reinterpret_cast<const float4*>(x + b * L.d + col);
+                        if (col < L.d) lo = __ldcg(src);
+                        if (col + 4 < L.d) hi = __ldcg(src + 1);
+                    }
+                    xr[b][j][0] = lo.x; xr[b][j][1] = lo.y; xr[b][j][2] = lo.z; xr[b][j][3] = lo.w;
+                    xr[b][j][4] = hi.x; xr[b][j][5] = hi.y; xr[b][j][6] = hi.z; xr[b][j][7] = hi.w;
                 }
-                xr[b][j][0] = lo.x; xr[b][j][1] = lo.y; xr[b][j][2] = lo.z; xr[b][j][3] = lo.w;
-                xr[b][j][4] = hi.x; xr[b][j][5] = hi.y; xr[b][j][6] = hi.z; xr[b][j][7] = hi.w;
             }
-        }
+        };
+        load_x();
+        float rms_inv[NB];  // the input RMS norm's per-sample scale (re-applied when x is reloaded)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) rms_inv[b] = 1.0f;
         unsigned prev_actives = 0;  // thread 0: the previous launch's active count (in flight)
         if (threadIdx.x == 0) {
 #ifdef CD_TIMELINE
@@ -427,6 +433,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 float ss = 0.0f;
                 for (int w = 0; w < nwc; ++w) ss += rms_red[w * NB + b];
                 const float inv = rsqrtf(ss / static_cast<float>(L.d) + P.rms_eps);
+                rms_inv[b] = inv;
 #pragma unroll
                 for (int j = 0; j < VPT; ++j)
 #pragma unroll
@@ -732,6 +739,18 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             TLF(5, 5);
         }
         if constexpr (!kSplit3) {
+        if constexpr (NB > 1) {
+            // x again (L2 hits, in flight while the first records stream in): not holding it in
+            // registers through stage 2 keeps the batch-2..4 variants from spilling there
+            load_x();
+            if (P.rms_eps >= 0.0f)
+#pragma unroll
+                for (int b = 0; b < NB; ++b)
+#pragma unroll
+                    for (int j = 0; j < VPT; ++j)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) xr[b][j][k] *= rms_inv[b];
+        }
         int st = 0;
         uint32_t ph = 0;
 

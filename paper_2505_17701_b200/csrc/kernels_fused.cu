@@ -135,8 +135,10 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
     // batch-1 bf16: stage 3 splits each record between one "dot" warp (u, g over the whole row
     // from shared memory, s = u act(g)) and the "down" warps (column-owned y += s W_down[i]),
     // handing s over through a per-stage mbarrier -- no CTA-wide barrier per record group
-    constexpr bool kSplit3 = kRegB && NB == 1;
-    constexpr int kVPD = 4;    // down-warp column vectors per thread (<= 4: d <= 32 x 8 x nd)
+    // (batch 2-4: when the columns fit one vector per consumer thread, VPT == 1 -- the down warps
+    // then hold NB x 2 vectors of y; the dot warps compute only the samples a record is alive for)
+    constexpr bool kSplit3 = kRegB && (NB == 1 || VPT == 1);
+    constexpr int kVPD = NB == 1 ? 4 : 2;  // down-warp column vectors per thread (<= kVPD x 8 x nd columns)
     const int nwc = blockDim.x / kWarp - 1;
     const int nc = nwc * kWarp;
     const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
@@ -166,8 +168,8 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
     float* rms_red = reinterpret_cast<float*>(cnt + NB + 4);   // [nwc][NB] sum-of-squares partials
     // split stage 3: per-stage s hand-over barriers and values, x as f32 for the dot warps
     uint64_t* sready = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(rms_red + nwc * NB) + 15) & ~uintptr_t(15));
-    float* svs = reinterpret_cast<float*>(sready + nstages);
-    float* xs = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(svs + nstages) + 15) & ~uintptr_t(15));
+    float* svs = reinterpret_cast<float*>(sready + nstages);  // [nstages][NB]
+    float* xs = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(svs + nstages * NB) + 15) & ~uintptr_t(15));
     const int n_dot = kSplit3 ? P.n_dot : 0;
 
     const int64_t c0 = (int64_t)blockIdx.x * rows_per_cta;
@@ -448,9 +450,12 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 if (vec < nvec) {
                     // two planes (elements 0-3 / 4-7 of every 8-vector): a dot warp's lanes then
                     // read consecutive 16-byte words (no 2-way bank conflict)
-                    float4* lo = reinterpret_cast<float4*>(xs);
-                    lo[vec] = make_float4(xr[0][j][0], xr[0][j][1], xr[0][j][2], xr[0][j][3]);
-                    lo[nvec + vec] = make_float4(xr[0][j][4], xr[0][j][5], xr[0][j][6], xr[0][j][7]);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {  // per sample: its two planes at b x ld floats
+                        float4* lo = reinterpret_cast<float4*>(xs) + b * 2 * nvec;
+                        lo[vec] = make_float4(xr[b][j][0], xr[b][j][1], xr[b][j][2], xr[b][j][3]);
+                        lo[nvec + vec] = make_float4(xr[b][j][4], xr[b][j][5], xr[b][j][6], xr[b][j][7]);
+                    }
                 }
             }
         }
@@ -928,29 +933,37 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
 #endif
                 const W* rup = reinterpret_cast<const W*>(ring + sq * stage_bytes);
                 const W* rgate = reinterpret_cast<const W*>(ring + sq * stage_bytes + row_bytes);
-                float u0 = 0.f, u1 = 0.f, g0 = 0.f, g1 = 0.f;
-#pragma unroll 4
-                for (int v = lane; v < nvec; v += kWarp) {
-                    float wu[8], wg[8];
-                    Vec8<W>::load(rup + v * kVec, wu);
-                    Vec8<W>::load(rgate + v * kVec, wg);
-                    const float4 xa = reinterpret_cast<const float4*>(xs)[v];
-                    const float4 xb = reinterpret_cast<const float4*>(xs)[nvec + v];
-                    const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+                const uint32_t bits = meta[sq].bits;
 #pragma unroll
-                    for (int k = 0; k < 8; k += 2) {
-                        ffma2(u0, u1, wu[k], wu[k + 1], xv[k], xv[k + 1]);
-                        ffma2(g0, g1, wg[k], wg[k + 1], xv[k], xv[k + 1]);
+                for (int b = 0; b < NB; ++b) {
+                    float sb = 0.0f;
+                    if ((bits >> b) & 1u) {  // (a record of the union: only its live samples)
+                        const float4* xp = reinterpret_cast<const float4*>(xs) + b * 2 * nvec;
+                        float u0 = 0.f, u1 = 0.f, g0 = 0.f, g1 = 0.f;
+#pragma unroll 4
+                        for (int v = lane; v < nvec; v += kWarp) {
+                            float wu[8], wg[8];
+                            Vec8<W>::load(rup + v * kVec, wu);
+                            Vec8<W>::load(rgate + v * kVec, wg);
+                            const float4 xa = xp[v];
+                            const float4 xb = xp[nvec + v];
+                            const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+                            for (int k = 0; k < 8; k += 2) {
+                                ffma2(u0, u1, wu[k], wu[k + 1], xv[k], xv[k + 1]);
+                                ffma2(g0, g1, wg[k], wg[k + 1], xv[k], xv[k + 1]);
+                            }
+                        }
+                        float v2[2] = {u0 + u1, g0 + g1};
+                        const float tot = warp_transpose_sum<2>(v2);  // lanes 0-15: u, 16-31: g
+                        const float gsum = __shfl_sync(0xffffffffu, tot, 16);
+                        sb = tot * act_fast(L.act, gsum);
                     }
+                    if (lane == 0) svs[sq * NB + b] = sb;
                 }
-                float v2[2] = {u0 + u1, g0 + g1};
-                const float tot = warp_transpose_sum<2>(v2);  // lanes 0-15: u, 16-31: g
-                const float gsum = __shfl_sync(0xffffffffu, tot, 16);
                 __syncwarp();
                 if (lane == 0) {
-                    const bool alive = meta[sq].bits & 1u;
-                    svs[sq] = alive ? tot * act_fast(L.act, gsum) : 0.0f;
-                    mbar_arrive(&sready[sq]);  // release-orders the s store for the down warps
+                    mbar_arrive(&sready[sq]);  // release-orders the s stores for the down warps
                     mbar_arrive(&empty[sq]);
                 }
             }
@@ -958,11 +971,13 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             // down warps: column vectors td + j nd of y, every record in sequence
             const int td = ct - n_dot * kWarp;
             const int nd = (nwc - n_dot) * kWarp;
-            float yd[kVPD][8];
+            float yd[NB][kVPD][8];
 #pragma unroll
-            for (int j = 0; j < kVPD; ++j)
+            for (int b = 0; b < NB; ++b)
 #pragma unroll
-                for (int k = 0; k < 8; ++k) yd[j][k] = 0.0f;
+                for (int j = 0; j < kVPD; ++j)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) yd[b][j][k] = 0.0f;
             int n_rec = 0;
             int sq = -1;
             uint32_t upar = 0;
@@ -970,7 +985,9 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 if (++sq == nstages) { sq = 0; upar ^= 1u; }
                 mbar_wait(&sready[sq], upar);
                 if (meta[sq].idx < 0) break;
-                const float sv = svs[sq];
+                float sv[NB];
+#pragma unroll
+                for (int b = 0; b < NB; ++b) sv[b] = svs[sq * NB + b];
                 const W* rdown = reinterpret_cast<const W*>(ring + sq * stage_bytes + 2 * row_bytes);
 #pragma unroll
                 for (int j = 0; j < kVPD; ++j) {
@@ -979,7 +996,10 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                         float wd[8];
                         Vec8<W>::load(rdown + vec * kVec, wd);
 #pragma unroll
-                        for (int k = 0; k < 8; k += 2) ffma2(yd[j][k], yd[j][k + 1], sv, sv, wd[k], wd[k + 1]);
+                        for (int b = 0; b < NB; ++b)
+#pragma unroll
+                            for (int k = 0; k < 8; k += 2)
+                                ffma2(yd[b][j][k], yd[b][j][k + 1], sv[b], sv[b], wd[k], wd[k + 1]);
                     }
                 }
                 __syncwarp();
@@ -997,16 +1017,20 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                     const int vec = td + j * nd;
                     if (vec < nvec) {
                         // d % 4 == 0 (launch requirement): whole float4s, 8 lanes per 128 bytes
-                        float4* dst = reinterpret_cast<float4*>(ys + (int64_t)vec * kVec);
-                        if ((int64_t)vec * kVec < L.d) dst[0] = make_float4(yd[j][0], yd[j][1], yd[j][2], yd[j][3]);
-                        if ((int64_t)vec * kVec + 4 < L.d) dst[1] = make_float4(yd[j][4], yd[j][5], yd[j][6], yd[j][7]);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            if (b >= nb) continue;
+                            float4* dst = reinterpret_cast<float4*>(ys + b * L.d + (int64_t)vec * kVec);
+                            if ((int64_t)vec * kVec < L.d) dst[0] = make_float4(yd[b][j][0], yd[b][j][1], yd[b][j][2], yd[b][j][3]);
+                            if ((int64_t)vec * kVec + 4 < L.d) dst[1] = make_float4(yd[b][j][4], yd[b][j][5], yd[b][j][6], yd[b][j][7]);
+                        }
                     }
                 }
                 fence_proxy_async_smem();
                 named_bar_sync(kBarD, nd);
                 if (td == 0) {
                     (void)await_acquire(S.t_count + kYZeroWord, tag);  // y zeroed
-                    bulk_reduce_add_f32(y, ys, static_cast<uint32_t>(L.d * sizeof(float)));
+                    bulk_reduce_add_f32(y, ys, static_cast<uint32_t>(nb * L.d * sizeof(float)));
                     bulk_commit_and_wait_read();
                 }
             }
@@ -1092,10 +1116,10 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     if (regb) nwc64 = std::max<int64_t>(nwc64, (rpc + 7) / 8);
     // split stage 3 (batch 1, bf16): 8 down warps own the columns (<= 4 vectors each), the
     // other consumer warps (>= 2) compute the records' dots
-    const bool split3 = regb && nbk == 1;
+    const bool split3 = regb && (nbk == 1 || vpt == 1);
     if (split3) nwc64 = std::max<int64_t>(nwc64, 10);
     const int nwc = static_cast<int>(nwc64);
-    if (split3 && (nvec + 8 * kWarp - 1) / (8 * kWarp) > 4) return cudaErrorInvalidValue;
+    if (split3 && (nvec + 8 * kWarp - 1) / (8 * kWarp) > (nbk == 1 ? 4 : 2)) return cudaErrorInvalidValue;
     if (nwc * kWarp > kMaxConsumers) return cudaErrorInvalidValue;
     const int threads = (nwc + 1) * kWarp;
     // fixed carve-up beside the ring: latent, barriers, meta, lists, scratch, latent fragments
@@ -1103,7 +1127,7 @@ cudaError_t launch_dc_fused(const LayerDev& L, const Scratch& S, const float* x,
     const int64_t aux_bytes = (int64_t)qrows * L.ld * esz;
     const int64_t fixed = (int64_t)nbk * L.ldr * 4 + 3 * 8 + (int64_t)rpc * 8 + (nwc * 32 + kGroupF * nbk) * 4 +
                           (4 + nbk) * 4 + nwc * nbk * 4 + 64 +
-                          (split3 ? 12 * 12 + L.ld * 4 + 32 : 0);  // s hand-over (<= 12 stages), x f32
+                          (split3 ? 12 * (8 + 4 * nbk) + nbk * L.ld * 4 + 32 : 0);  // s hand-over, x f32
     const int64_t per_stage = stage_bytes + 2 * 8 + (int64_t)sizeof(MetaF);
     const int nstages = static_cast<int>(imin64(12, (kSmemBudgetF - fixed) / per_stage));
     if (nstages < 2) return cudaErrorInvalidValue;

@@ -51,6 +51,9 @@ using namespace fused;
 #ifndef CD_PF_EARLY
 #define CD_PF_EARLY 1  // next-layer predictor prefetch issued at the start of the chain (0: behind the records)
 #endif
+#ifndef CD_A_FIRST
+#define CD_A_FIRST 1  // theta_b copy issued only after theta_a landed (theta_a gates stage 1)
+#endif
 
 constexpr int kRBf = 8;       // predictor rows per warp iteration (stage 2)
 constexpr int kGroupF = 4;    // neurons per reduction round (stage 3)
@@ -211,6 +214,9 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             }
             if ((!kRegB || P.b_smem) && nrows > 0) {
                 // the chunk's predictor rows: one bulk copy into the (idle) ring head
+#if CD_A_FIRST
+                if (nq > 0) mbar_wait(bar_a, 0);  // theta_a gates stage 1: let it land first
+#endif
                 const int64_t bytes = nrows * brow_bytes;
                 mbar_arrive_expect_tx(bar_b, static_cast<uint32_t>(bytes));
                 bulk_g2s(ring, BT + c0 * brow_bytes, static_cast<uint32_t>(bytes), bar_b, pol);

@@ -54,6 +54,21 @@ __device__ __forceinline__ uint4 ldg_early_v4(const void* p) {
     return v;
 }
 
+// 8 consecutive f32 (an activation 8-vector) bypassing L1: one 256-bit load (LDG.256) when the
+// vector is whole and 32-byte aligned -- a warp's request is then 1 KB of consecutive sectors
+// instead of two half-efficient 16-byte passes -- else per-float4 loads of what lies below `avail`
+__device__ __forceinline__ void ldcg_x8(const float* p, int64_t avail, float4& lo, float4& hi) {
+    if (avail >= 8 && (reinterpret_cast<uintptr_t>(p) & 31u) == 0) {
+        asm volatile("ld.global.cg.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+                     : "l"(p));
+        return;
+    }
+    const float4* src = reinterpret_cast<const float4*>(p);
+    if (avail > 0) lo = __ldcg(src);
+    if (avail > 4) hi = __ldcg(src + 1);
+}
+
 __device__ __forceinline__ unsigned long long tagged(uint32_t tag, uint32_t payload) {
     return (static_cast<unsigned long long>(tag) << 32) | payload;
 }

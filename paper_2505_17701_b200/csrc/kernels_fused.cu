@@ -385,11 +385,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 for (int b = 0; b < NB; ++b) {
                     float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
                     const int64_t col = (int64_t)vec * kVec;
-                    if (vec < nvec && b < nb) {
-                        const float4* src = reinterpret_cast<const float4*>(x + b * L.d + col);
-                        if (col < L.d) lo = __ldcg(src);
-                        if (col + 4 < L.d) hi = __ldcg(src + 1);
-                    }
+                    if (vec < nvec && b < nb) ldcg_x8(x + b * L.d + col, L.d - col, lo, hi);
                     xr[b][j][0] = lo.x; xr[b][j][1] = lo.y; xr[b][j][2] = lo.z; xr[b][j][3] = lo.w;
                     xr[b][j][4] = hi.x; xr[b][j][5] = hi.y; xr[b][j][6] = hi.z; xr[b][j][7] = hi.w;
                 }

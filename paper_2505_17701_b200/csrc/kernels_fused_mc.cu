@@ -219,11 +219,7 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
             const int vec = ct + j * nc;
             float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
             const int64_t col = (int64_t)vec * kVec;
-            if (vec < nvec) {
-                const float4* src = reinterpret_cast<const float4*>(P.x + col);
-                if (col < L.d) lo = __ldcg(src);
-                if (col + 4 < L.d) hi = __ldcg(src + 1);
-            }
+            if (vec < nvec) ldcg_x8(P.x + col, L.d - col, lo, hi);
             xr[j][0] = lo.x; xr[j][1] = lo.y; xr[j][2] = lo.z; xr[j][3] = lo.w;
             xr[j][4] = hi.x; xr[j][5] = hi.y; xr[j][6] = hi.z; xr[j][7] = hi.w;
         }

@@ -462,11 +462,16 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             }
         }
 #ifdef CD_TIMELINE
-        if (threadIdx.x == 0) {
+        long long tl_xw = 0;
+        if (lane == 0) {
+            // per-warp x arrival (clock64): warps 0-7 in row 3, 8-15 in row 7
 #pragma unroll
             for (int j = 0; j < VPT; ++j)
 #pragma unroll
                 for (int k = 0; k < 8; ++k) asm volatile("" ::"f"(xr[0][j][k]));
+            tl_xw = clock64();  // written once the launch tag is known (below)
+        }
+        if (threadIdx.x == 0) {
             TLF(0, 0);
             TLC(1);
         }
@@ -483,6 +488,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
 #ifdef CD_TIMELINE
         tl_tag = tag;
+        if (lane == 0 && blockIdx.x < kTlCtas) g_tlf[tl_tag & 3u][warp < 8 ? 3 : 7][blockIdx.x][warp & 7] = tl_xw;
 #endif
         if (threadIdx.x == 0) { TLF(6, 2); TLC(2); }
 
@@ -493,27 +499,56 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             constexpr int kQ = 4;
             for (int qb = 0; qb < nq; qb += kQ) {
                 float v[kQ * NB];
+                if constexpr (NB * VPT > 2 || VPL > 2) {
+                    // (register-heavy variants: rows one at a time, no hoisting -- avoids spills)
 #pragma unroll
-                for (int qq = 0; qq < kQ; ++qq) {
-                    float a0[NB], a1[NB];
+                    for (int qq = 0; qq < kQ; ++qq) {
+                        float a0[NB], a1[NB];
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0f;
-                    if (qb + qq < nq) {
+                        for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0f;
+                        if (qb + qq < nq) {
 #pragma unroll
-                        for (int j = 0; j < VPT; ++j) {
-                            const int vec = ct + j * nc;
-                            if (vec < nvec) {
-                                float w[8];
-                                Vec8<W>::load(abuf + (int64_t)(qb + qq) * L.ld + vec * kVec, w);
+                            for (int j = 0; j < VPT; ++j) {
+                                const int vec = ct + j * nc;
+                                if (vec < nvec) {
+                                    float w[8];
+                                    Vec8<W>::load(abuf + (int64_t)(qb + qq) * L.ld + vec * kVec, w);
 #pragma unroll
-                                for (int b = 0; b < NB; ++b)
+                                    for (int b = 0; b < NB; ++b)
 #pragma unroll
-                                    for (int k = 0; k < 8; k += 2) ffma2(a0[b], a1[b], w[k], w[k + 1], xr[b][j][k], xr[b][j][k + 1]);
+                                        for (int k = 0; k < 8; k += 2) ffma2(a0[b], a1[b], w[k], w[k + 1], xr[b][j][k], xr[b][j][k + 1]);
+                                }
                             }
                         }
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) v[qq * NB + b] = a0[b] + a1[b];
+                    }
+                } else {
+                    // branch-free: every row / vector read is issued before the first FMA (clamped
+                    // indices; x is zero past the end, and rows past nq are never published)
+                    float w[kQ][VPT][8];
+#pragma unroll
+                    for (int qq = 0; qq < kQ; ++qq) {
+                        const int row = min(qb + qq, nq - 1);
+#pragma unroll
+                        for (int j = 0; j < VPT; ++j)
+                            Vec8<W>::load(abuf + (int64_t)row * L.ld + min(ct + j * nc, nvec - 1) * kVec, w[qq][j]);
                     }
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) v[qq * NB + b] = a0[b] + a1[b];
+                    for (int qq = 0; qq < kQ; ++qq) {
+                        float a0[NB], a1[NB];
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) a0[b] = a1[b] = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < VPT; ++j)
+#pragma unroll
+                            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                                for (int k = 0; k < 8; k += 2)
+                                    ffma2(a0[b], a1[b], w[qq][j][k], w[qq][j][k + 1], xr[b][j][k], xr[b][j][k + 1]);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) v[qq * NB + b] = a0[b] + a1[b];
+                    }
                 }
                 constexpr int kV = kQ * NB;
                 if (threadIdx.x == 0 && qb == 0) { TLF(0, 1); TLC(4); }

@@ -434,8 +434,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             named_bar_sync(kBarC, nc);
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-                float ss = 0.0f;
-                for (int w = 0; w < nwc; ++w) ss += rms_red[w * NB + b];
+                const float ss = warp_sum(lane < nwc ? rms_red[lane * NB + b] : 0.0f);  // nwc <= 32
                 const float inv = rsqrtf(ss / static_cast<float>(L.d) + P.rms_eps);
                 rms_inv[b] = inv;
 #pragma unroll
@@ -556,15 +555,24 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
                 named_bar_sync(kBarC, nc);
                 if (threadIdx.x == 0 && qb == 0) { TLF(0, 2); TLC(5); }
-                if (warp == 0 && lane < kV) {
-                    const int qq = lane / NB, b = lane % NB;
+                if (warp == 0) {
+                    // the nwc warp partials of value vv: lane group g sums warps g, g + kG, ..., an
+                    // xor butterfly over the groups leaves the total in every lane of column vv,
+                    // and group g then publishes replicas g, g + kG, ... (no serial 13-term chain)
+                    constexpr int kG = 32 / kV;
+                    const int vv = lane % kV, g = lane / kV;
                     float s = 0.0f;
-                    for (int w = 0; w < nwc; ++w) s += red[w * 32 + lane];
+                    for (int w = g; w < nwc; w += kG) s += red[w * 32 + vv];
+#pragma unroll
+                    for (int o = kV; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    const int qq = vv / NB, b = vv % NB;
                     if (qb + qq < nq && b < nb)
-                        for (int rp = 0; rp < P.lat_rep; ++rp)
+                        for (int rp = g; rp < P.lat_rep; rp += kG)
                             st_relaxed_u64(S.t_lat + (int64_t)rp * NB * L.ldr + b * L.ldr + q0 + qb + qq,
                                            tagged(tag, __float_as_uint(s)));
                 }
+                // (also keeps the other warps' latent polls off the L2 until this CTA's
+                // columns are out: polling early measured slower)
                 named_bar_sync(kBarC, nc);
                 if (threadIdx.x == 0 && qb == 0) { TLF(0, 3); TLC(6); }
             }

@@ -56,12 +56,10 @@ cyc = tl[2].copy()
 xw = np.concatenate([tl[3], tl[7]], axis=1)[:, :16].astype(np.int64)  # per-warp x arrival (clock64)
 tl[3] = 0
 tl[7] = 0
-okx = (cyc[:, 0] > 0) & (xw[:, :15] > 0).all(axis=1)
-if okx.any():
-    rel = xw[okx, :15] - cyc[okx, 0:1]
-    print("  per-warp x arrival after thread 0's wait mark (cycles): warp median over CTAs / CTA-max-warp p50,p90:",
-          " ".join(f"{np.median(rel[:, w]):.0f}" for w in range(15)), "/",
-          f"{np.median(rel.max(axis=1)):.0f},{np.percentile(rel.max(axis=1), 90):.0f}")
+rel = np.where((xw > 0) & (cyc[:, 0:1] > 0), xw - cyc[:, 0:1], np.iinfo(np.int64).min)
+print("  per-warp x arrival after thread 0's wait mark (cycles, median over CTAs; n):",
+      " ".join(f"{np.median(rel[rel[:, w] > -10**12, w]):.0f}({(rel[:, w] > -10**12).sum()})"
+               if (rel[:, w] > -10**12).any() else "-" for w in range(16)))
 tl[2] = 0
 ok = (cyc[:, 0] > 0) & (cyc[:, 7] > 0)
 if ok.any():

@@ -69,6 +69,22 @@ __device__ __forceinline__ void ldcg_x8(const float* p, int64_t avail, float4& l
     if (avail > 4) hi = __ldcg(src + 1);
 }
 
+// Column sums of nw warp partials part[w * stride + v], v < V (V a power of two <= 32), by one
+// whole warp: lane group g = lane / V adds warps g, g + 32/V, ..., then an xor butterfly over the
+// groups -- every lane returns the total of column lane % V (a few shuffles instead of an
+// nw-long chain of dependent shared loads)
+template <int V>
+__device__ __forceinline__ float sum_partials(const float* part, int stride, int nw, int lane) {
+    static_assert(V >= 1 && V <= 32 && (V & (V - 1)) == 0, "V must be a power of two <= 32");
+    constexpr int kG = 32 / V;
+    const int v = lane % V;
+    float s = 0.0f;
+    for (int w = lane / V; w < nw; w += kG) s += part[w * stride + v];
+#pragma unroll
+    for (int o = V; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
 __device__ __forceinline__ unsigned long long tagged(uint32_t tag, uint32_t payload) {
     return (static_cast<unsigned long long>(tag) << 32) | payload;
 }

@@ -556,15 +556,11 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 named_bar_sync(kBarC, nc);
                 if (threadIdx.x == 0 && qb == 0) { TLF(0, 2); TLC(5); }
                 if (warp == 0) {
-                    // the nwc warp partials of value vv: lane group g sums warps g, g + kG, ..., an
-                    // xor butterfly over the groups leaves the total in every lane of column vv,
-                    // and group g then publishes replicas g, g + kG, ... (no serial 13-term chain)
+                    // every lane of column vv holds its total; lane group g publishes replicas
+                    // g, g + 32/kV, ...
                     constexpr int kG = 32 / kV;
                     const int vv = lane % kV, g = lane / kV;
-                    float s = 0.0f;
-                    for (int w = g; w < nwc; w += kG) s += red[w * 32 + vv];
-#pragma unroll
-                    for (int o = kV; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    const float s = sum_partials<kV>(red, 32, nwc, lane);
                     const int qq = vv / NB, b = vv % NB;
                     if (qb + qq < nq && b < nb)
                         for (int rp = g; rp < P.lat_rep; rp += kG)
@@ -873,18 +869,18 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             const float tot = warp_transpose_sum<kV>(v);
             if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
             named_bar_sync(kBarC, nc);
-            if (warp == 0 && lane < ns * NB) {
+            if (warp == 0) {
+                const float col = sum_partials<kV>(red, 32, nwc, lane);  // column lane % kV
                 const int q = lane / NB, b = lane % NB;
-                float g = 0.0f, u = 0.0f;
-                for (int w = 0; w < nwc; ++w) {
-                    g += red[w * 32 + (q * 2) * NB + b];
-                    u += red[w * 32 + (q * 2 + 1) * NB + b];
-                }
-                int sq = sts[0];
+                const float g = __shfl_sync(0xffffffffu, col, ((q * 2) * NB + b) % kV);
+                const float u = __shfl_sync(0xffffffffu, col, ((q * 2 + 1) * NB + b) % kV);
+                if (lane < ns * NB) {
+                    int sq = sts[0];
 #pragma unroll
-                for (int qq = 1; qq < kGroupF; ++qq) sq = (q == qq) ? sts[qq] : sq;
-                const bool alive = (meta[sq].bits >> b) & 1u;
-                sval[lane] = alive ? u * act_fast(L.act, g) : 0.0f;
+                    for (int qq = 1; qq < kGroupF; ++qq) sq = (q == qq) ? sts[qq] : sq;
+                    const bool alive = (meta[sq].bits >> b) & 1u;
+                    sval[lane] = alive ? u * act_fast(L.act, g) : 0.0f;
+                }
             }
             named_bar_sync(kBarC, nc);
 #pragma unroll

@@ -293,9 +293,7 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
                 const int s = s0 + (lane >> 2), q = lane & 3;
                 const int64_t r0 = c0 + (int64_t)s * rps;
                 const bool valid = lane < 4 * kSG && s < nst_u && q < 3 && r0 + q < c1;
-                float u = 0.0f;
-                if (valid)
-                    for (int w = 0; w < nwc; ++w) u += rb[w * 16 + lane];
+                const float u = sum_partials<16>(rb, 16, nwc, lane);  // column lane (lane < 16)
                 const int64_t gi = r0 + q;
                 bool a = false;
                 if (valid) {
@@ -366,13 +364,14 @@ __global__ void __launch_bounds__(544, 1) k_mc_fused(const __grid_constant__ Fus
             const float tot = warp_transpose_sum<kGroupM>(v);
             if ((lane & 7) == 0) red[warp * 32 + (lane >> 3)] = tot;
             named_bar_sync(kBarC, nc);
-            if (warp == 0 && lane < ns) {
-                float g = 0.0f;
-                for (int w = 0; w < nwc; ++w) g += red[w * 32 + lane];
-                int sq = sts[0];
+            if (warp == 0) {
+                const float g = sum_partials<kGroupM>(red, 32, nwc, lane);
+                if (lane < ns) {
+                    int sq = sts[0];
 #pragma unroll
-                for (int qq = 1; qq < kGroupM; ++qq) sq = (lane == qq) ? sts[qq] : sq;
-                sval[lane] = act_fast(L.act, g) * meta[sq].u;
+                    for (int qq = 1; qq < kGroupM; ++qq) sq = (lane == qq) ? sts[qq] : sq;
+                    sval[lane] = act_fast(L.act, g) * meta[sq].u;
+                }
             }
             named_bar_sync(kBarC, nc);
 #pragma unroll

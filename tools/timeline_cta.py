@@ -53,13 +53,13 @@ g.replay()
 torch.cuda.synchronize()
 tl = read()[:, :148]
 cyc = tl[2].copy()
-xw = np.concatenate([tl[3], tl[7]], axis=1)[:, :16].astype(np.int64)  # per-warp x arrival (clock64)
+xw = np.concatenate([tl[3], tl[7]], axis=1)[:, :13].astype(np.int64)  # per-warp x arrival (clock64)
 tl[3] = 0
 tl[7] = 0
 rel = np.where((xw > 0) & (cyc[:, 0:1] > 0), xw - cyc[:, 0:1], np.iinfo(np.int64).min)
 print("  per-warp x arrival after thread 0's wait mark (cycles, median over CTAs; n):",
       " ".join(f"{np.median(rel[rel[:, w] > -10**12, w]):.0f}({(rel[:, w] > -10**12).sum()})"
-               if (rel[:, w] > -10**12).any() else "-" for w in range(16)))
+               if (rel[:, w] > -10**12).any() else "-" for w in range(13)))
 tl[2] = 0
 ok = (cyc[:, 0] > 0) & (cyc[:, 7] > 0)
 if ok.any():

@@ -269,7 +269,11 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         const int n_own = cnt[0];
         const int kept = min(n_own, cnt[NB + 2]);
         const int ovf = n_own - kept;
-        unsigned* qc = S.ctl + kCtlQueue + (tag % 3u) * 32u;  // [0] tail [1] head [2] pushed [3] actives
+        // [0..1] one 64-bit word {tail (low), pushed CTAs (high)}: a single load is a consistent
+        // snapshot of both, so "all pushed" and the final tail arrive in one round trip.
+        // [2] head (steal claims) [3] actives
+        unsigned* qc = S.ctl + kCtlQueue + (tag % 3u) * 32u;
+        unsigned long long* qtp = reinterpret_cast<unsigned long long*>(qc);
         int e = 0;
         if (lane == 0) {
             TLF(6, 5);
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         int base = 0;
         if (lane == 0) {
             red_add_u32(qc + 3, static_cast<unsigned>(n_own));
-            if (ovf > 0) base = static_cast<int>(atomicAdd(qc + 0, static_cast<unsigned>(ovf)));
+            if (ovf > 0) base = static_cast<int>(atomicAdd(qtp, static_cast<unsigned long long>(ovf)) & 0xFFFFFFFFull);
         }
         base = __shfl_sync(0xffffffffu, base, 0);
         for (int k = lane; k < ovf; k += kWarp) {
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
         }
         __syncwarp();
         if (lane == 0) {
-            red_add_u32(qc + 2, 1u);  // pushed (stealers check each entry's tag, no ordering needed)
+            atomicAdd(qtp, 1ull << 32);  // pushed (after this CTA's tail reservation returned)
             TLF(6, 6);
             for (; e < kept; ++e) issue(own_idx[e], own_bits[e]);
             TLF(1, 1);
@@ -309,25 +313,26 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
             const unsigned G_u = static_cast<unsigned>(G);
             unsigned tail_final = 0xFFFFFFFFu;
             int n_stolen = 0;
-            unsigned next = atomicAdd(qc + 1, 1u);
+            unsigned next = atomicAdd(qc + 2, 1u);
             for (;;) {
                 const unsigned slot = next;
                 bool got = false;
                 uint32_t wv = 0;
                 while (slot < tail_final) {
-                    if (slot < static_cast<unsigned>(L.F)) {
-                        const unsigned long long w = ld_relaxed_u64(S.t_list + slot);
-                        if (static_cast<uint32_t>(w >> 32) == tag) {
-                            wv = static_cast<uint32_t>(w);
-                            got = true;
-                            break;
-                        }
+                    // the entry and the {tail, pushed} snapshot in flight together
+                    const bool in_list = slot < static_cast<unsigned>(L.F);
+                    const unsigned long long w = in_list ? ld_relaxed_u64(S.t_list + slot) : 0ull;
+                    const unsigned long long tp = ld_relaxed_u64(qtp);
+                    if (in_list && static_cast<uint32_t>(w >> 32) == tag) {
+                        wv = static_cast<uint32_t>(w);
+                        got = true;
+                        break;
                     }
-                    // every CTA's tail reservation returned before it counted itself as pushed
-                    if (ld_relaxed_u32(qc + 2) == G_u) tail_final = ld_relaxed_u32(qc + 0);
+                    // every CTA's tail reservation precedes its push in the word's order
+                    if (static_cast<unsigned>(tp >> 32) == G_u) tail_final = static_cast<unsigned>(tp);
                 }
                 if (!got) break;
-                next = atomicAdd(qc + 1, 1u);
+                next = atomicAdd(qc + 2, 1u);
                 issue(static_cast<int32_t>(wv & ((1u << 27) - 1u)), wv >> 27);
                 if (n_stolen++ == 0) TLF(1, 2);
                 TLF(1, 3);

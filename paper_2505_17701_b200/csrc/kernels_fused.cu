@@ -488,12 +488,11 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 st_relaxed_u64(S.t_count + kYZeroWord, tagged(static_cast<uint32_t>(cnt[NB + 1]), 1u));
             }
         }
-        named_bar_sync(kBarC, nc);
-        const uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);
-#ifdef CD_TIMELINE
-        tl_tag = tag;
-        if (lane == 0 && blockIdx.x < kTlCtas) g_tlf[tl_tag & 3u][warp < 8 ? 3 : 7][blockIdx.x][warp & 7] = tl_xw;
-#endif
+        // the launch tag (thread 0's read) reaches the other threads through stage 1's first
+        // barrier -- none of its own, so every warp starts on its latent columns as soon as its x
+        // and theta_a are in
+        if (nq == 0) named_bar_sync(kBarC, nc);
+        uint32_t tag = static_cast<uint32_t>(cnt[NB + 1]);  // nq > 0: re-read after that barrier
         if (threadIdx.x == 0) { TLF(6, 2); TLC(2); }
 
         // ---------------------------------------------------------- stage 1: latent columns
@@ -559,6 +558,7 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 const float tot = warp_transpose_sum<kV>(v);
                 if ((lane % (32 / kV)) == 0) red[warp * 32 + lane / (32 / kV)] = tot;
                 named_bar_sync(kBarC, nc);
+                tag = static_cast<uint32_t>(cnt[NB + 1]);
                 if (threadIdx.x == 0 && qb == 0) { TLF(0, 2); TLC(5); }
                 if (warp == 0) {
                     // every lane of column vv holds its total; lane group g publishes replicas
@@ -578,6 +578,10 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 if (threadIdx.x == 0 && qb == 0) { TLF(0, 3); TLC(6); }
             }
         }
+#ifdef CD_TIMELINE
+        tl_tag = tag;
+        if (lane == 0 && blockIdx.x < kTlCtas) g_tlf[tl_tag & 3u][warp < 8 ? 3 : 7][blockIdx.x][warp & 7] = tl_xw;
+#endif
         if (threadIdx.x == 0) TLF(5, 2);
         if (kRegB && P.b_smem) {
             // predictor rows smem -> registers while the latent columns of the other CTAs arrive

@@ -615,11 +615,21 @@ __global__ void __launch_bounds__(512, 1) k_dc_fused(const __grid_constant__ Fus
                 const int q = e - b * (int)L.ldr;
                 w[k] = (e < NB * (int)L.ldr && b < nb && q < L.r) ? ld_relaxed_u64(t_lat + e) : tagged(tag, 0u);
             }
+            // stale words re-polled together (one round trip per pass for all of a thread's words,
+            // not one wait after another)
+            for (;;) {
+                bool stale = false;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) stale |= static_cast<uint32_t>(w[k] >> 32) != tag;
+                if (!stale) break;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (static_cast<uint32_t>(w[k] >> 32) != tag) w[k] = ld_relaxed_u64(t_lat + e0 + k * nc);
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int e = e0 + k * nc;
                 if (e >= NB * (int)L.ldr) continue;
-                if (static_cast<uint32_t>(w[k] >> 32) != tag) w[k] = tagged(tag, await_relaxed(t_lat + e, tag));
                 // two planes per sample (elements 0-3 / 4-7 of every 8-vector): the stage-2 reads
                 // of a warp are then consecutive 16-byte words (no 2-way bank conflict)
                 int b = 0;
